@@ -1,0 +1,395 @@
+"""Benchmark: preprocessed samples/s per box of the locality-aware loader.
+
+Workload (BASELINE.json configs[1], weak-scaled so N=1 fits one B200):
+  "cfg2-weak": synthetic ImageNet-1K-shaped u8 HWC 256x256x3 samples,
+  d = 160,000 * N (== 1.28 M at N = 8), one learner per GPU (p = N), global
+  batch 1024 * N (1,024 per GPU), full cache (alpha = 1: each GPU holds its
+  160,000-sample CacheDirectory block = 31.5 GB in HBM), locality-aware
+  balanced assignment, crop 224 + h-flip + ImageNet normalise -> NCHW fp32.
+  A step = exchange + augment of one global batch; the epoch plan
+  (permutation + assignment of all 156 steps) runs inside the timed region at
+  every epoch boundary (timed region starts at one).  Inputs (31.5 GB shard,
+  616 MB output per step) are far larger than L2, so no flush is needed.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "preprocessed samples/sec/box"
+PER_GPU_D = 160_000
+PER_GPU_B = 1024
+H = W = 256
+CROP = 224
+SEED = 42
+SRC_BYTES = CROP * CROP * 3                    # crop window read per sample
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "augment_crop_traffic.json")
+
+
+def out_bytes(dtype: str) -> int:
+    return 3 * CROP * CROP * (4 if dtype == "fp32" else 2)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1560)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--per-gpu-d", type=int, default=PER_GPU_D)
+    ap.add_argument("--per-gpu-batch", type=int, default=PER_GPU_B)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    return ap.parse_args()
+
+
+def workload(args, n):
+    return {"workload": "cfg2-weak: ImageNet-1K-shaped synthetic u8 256x256x3, "
+                        f"d={args.per_gpu_d}*N, p=N, global batch {args.per_gpu_batch}*N, "
+                        "alpha=1, locality_balanced, crop224+flip+normalize -> NCHW "
+                        f"{args.dtype}",
+            "d": args.per_gpu_d * n, "learners": n, "global_batch": args.per_gpu_batch * n,
+            "per_gpu_batch": args.per_gpu_batch, "alpha": 1.0, "scheme": "locality_balanced",
+            "exchange": args.exchange if n > 1 else "none", "out_dtype": args.dtype,
+            "l2": "inputs larger than L2 (31.5 GB shard, 616 MB output/step); no flush",
+            "timed_region": "starts at an epoch boundary; epoch plans included"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML (the library nvidia-smi reads) polled every ~2 ms in a thread."""
+    NAMES = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+             0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+             0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples = []
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        mask = 0
+        for _, r in self.samples:
+            mask |= r
+        reasons = sorted({n for b, n in self.NAMES.items() if mask & b})
+        mhz = [m for m, _ in self.samples]
+        return {"sm_mhz": float(np.median(mhz)) if mhz else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(mhz),
+                "source": "NVML"}
+
+
+# ------------------------------------------------------------------ CPU arm
+def cpu_reference_run(args, n, steps, warmup, seconds_cap=None):
+    """The reference's CPU path: oracle/_ref (the unmodified reference sources:
+    permute_epoch, loc_distribution + targets + balance + tail moves) for the
+    plan, and the oracle's C augment restatement on every host thread (the
+    reference has no augment; its Loader 'preprocess' is an injected sleep).
+    Samples come from a warm host cache: a pool of 4,096 generate_dataset
+    samples, sample id s served from slot s mod 4096."""
+    import oracle
+    d, B = args.per_gpu_d * n, args.per_gpu_batch * n
+    spe = d // B
+    pool_n = 4096
+    pool = np.stack([oracle.gen_sample(SEED, i, H * W * 3) for i in range(pool_n)])
+    cores = len(os.sched_getaffinity(0))
+    chunk = min(B, 1024)
+    out = np.empty(chunk * out_bytes(args.dtype), np.uint8)
+    bf16 = args.dtype == "bf16"
+    cache = {"epoch": None, "order": None}
+
+    def one_step(t):
+        e, s = divmod(t, spe)
+        if cache["epoch"] != e:
+            cache["order"] = oracle.ref_permute_epoch(SEED, e, d)  # core.cpp:11-27
+            cache["epoch"] = e
+        batch = cache["order"][s * B:(s + 1) * B]
+        lists, off, _ = oracle.ref_assign_balanced(batch, d, n)    # sampling+balance
+        for c0 in range(0, B, chunk):
+            oracle.cpu_crop_step(pool, lists[c0:c0 + chunk], H, W, SEED, e, out, bf16, cores)
+        return B
+
+    for t in range(warmup):
+        one_step(t)
+    t0 = time.perf_counter()
+    done = samples = 0
+    start = ((warmup + spe - 1) // spe) * spe
+    for k in range(steps):
+        samples += one_step(start + k)
+        done += 1
+        if seconds_cap and time.perf_counter() - t0 > seconds_cap:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": samples / dt, "unit": "samples/s", "cores": cores, "steps": done,
+            "seconds": dt}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    n = args.gpus
+    if rank != 0:
+        return
+    r = cpu_reference_run(args, n, args.steps, args.warmup, seconds_cap=None)
+    sample = (f"{r['steps']} steps x {args.per_gpu_batch * n} samples of the workload on "
+              f"{r['cores']} host threads (warm host cache of 4096 samples)")
+    line = {"metric": METRIC, "value": r["value"], "unit": "samples/s", "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * r["seconds"] / max(r["steps"], 1), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": workload(args, n), "impl": "reference",
+            "cpu_baseline": {"value": r["value"], "unit": "samples/s", "cores": r["cores"],
+                             "kind": "reference", "sample": sample},
+            "e2e": {"value": r["value"], "unit": "samples/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_ours(args):
+    import torch
+    import paper_1910_01196_b200 as ll
+    from paper_1910_01196_b200 import _capi
+    from paper_1910_01196_b200.loader import AugmentConfig, DeviceLoader, LoaderConfig
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.gpus
+    assert world == n, f"--gpus {n} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    d, B = args.per_gpu_d * n, args.per_gpu_batch * n
+    cfg = LoaderConfig(d=d, height=H, width=W, learners=n, rank=rank, batch_size=B, alpha=1.0,
+                       seed=SEED, data_seed=SEED, scheme="locality_balanced",
+                       exchange=args.exchange if n > 1 else "none", prefetch_depth=2,
+                       augment=AugmentConfig(out_dtype=args.dtype))
+    ld = DeviceLoader(cfg, device=local)
+    ld.populate()                                   # K1: this learner's shard in HBM
+    if n > 1:
+        if args.exchange == "p2p":
+            handles = [None] * n
+            dist.all_gather_object(handles, ld.ipc_handle())
+            ld.open_peers(handles)
+        else:
+            uid = [DeviceLoader.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            ld.comm_init(uid[0])
+    spe = ld.steps_per_epoch
+    lib = _capi.lib()
+    ctx = ld.ctx
+    sp = C.c_size_t()
+    _capi.check(lib.ll_ctx_stream(ctx, C.byref(sp)))
+    stream = torch.cuda.ExternalStream(sp.value, device=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def run_steps(t0, k):
+        local_samples = 0
+        for t in range(t0, t0 + k):
+            e, s = divmod(t, spe)
+            info = ld.step(e, s)
+            local_samples += info.n_local
+        return local_samples
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        v = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    def sum_over_ranks(x):
+        if dist is None:
+            return x
+        v = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(v, op=dist.ReduceOp.SUM)
+        return float(v.item())
+
+    # warm-up: W steps of epoch 0 (and beyond)
+    run_steps(0, args.warmup)
+    start = ((args.warmup + spe - 1) // spe) * spe     # next epoch boundary
+    barrier()
+
+    # ---- timed region (value) ----
+    launches0 = C.c_uint64()
+    _capi.check(lib.ll_ctx_launch_count(ctx, C.byref(launches0)))
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        samples = run_steps(start, args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+        barrier()
+    launches1 = C.c_uint64()
+    _capi.check(lib.ll_ctx_launch_count(ctx, C.byref(launches1)))
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    total_samples = sum_over_ranks(samples)
+    value = total_samples / (ms / 1e3)
+
+    # ---- dominant kernel: live CUDA-event timing of augment_crop ----
+    _capi.check(lib.ll_ctx_reset_stats(ctx))
+    _capi.check(lib.ll_ctx_set_timing(ctx, 1))
+    k2 = min(args.steps, 2 * spe)
+    barrier()
+    run_steps(start, k2)
+    barrier()
+    _capi.check(lib.ll_ctx_set_timing(ctx, 0))
+    stats = {}
+    for name in ["augment_crop", "permute", "assign", "pack"]:
+        cnt, tot = C.c_uint64(), C.c_double()
+        _capi.check(lib.ll_ctx_kernel_stats(ctx, name.encode(), C.byref(cnt), C.byref(tot)))
+        stats[name] = (cnt.value, tot.value)
+    aug_n, aug_ms = stats["augment_crop"]
+    per_launch_bytes = args.per_gpu_batch * (SRC_BYTES + out_bytes(args.dtype))
+    achieved = per_launch_bytes / (aug_ms / aug_n / 1e3) / 1e9 if aug_n else 0.0
+    achieved = max_over_ranks(-achieved) * -1 if dist is not None else achieved  # min over ranks
+    peak = 6544.3
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        peak, peak_src = 6650.0, "B200_PROFILING.md fallback"
+    traffic = None
+    try:
+        with open(PROFILE_SUMMARY) as f:
+            prof = json.load(f)
+        if prof.get("dtype") == args.dtype and prof.get("per_gpu_batch") == args.per_gpu_batch:
+            traffic = prof["dram_bytes_per_launch"]
+    except Exception:
+        pass
+
+    # ---- e2e: reference-facing host call, host buffers, copies in the region ----
+    e2e = None
+    if not args.no_e2e:
+        pinned_batch = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        pinned_ids = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        k_e2e = min(args.steps, 2 * spe)
+        h2d = d2h = 0
+        barrier()
+        t0 = time.perf_counter()
+        e_cur = None
+        order = None
+        for t in range(start, start + k_e2e):
+            e, s = divmod(t, spe)
+            if e != e_cur:
+                order = ll.permute_epoch(SEED, e, d, device=local).order  # device plan, D2H
+                d2h += 8 * d
+                e_cur = e
+            pinned_batch[:] = order[s * B:(s + 1) * B]
+            info = ld.step_host(e, s, pinned_batch, pinned_ids)
+            h2d += 8 * B
+            d2h += 8 * info.n_local
+        barrier()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": sum_over_ranks(k_e2e * args.per_gpu_batch) / wall, "unit": "samples/s",
+               "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e,
+               "steps": k_e2e,
+               "path": "ll_loader_step_host (GlobalBatch ids from pinned host -> device "
+                       "assign/exchange/augment -> local ids to host) + ll_permute_epoch "
+                       "D2H per epoch"}
+
+    # ---- CPU baseline (rank 0, N = 1) ----
+    cpu = None
+    if rank == 0 and n == 1 and not args.no_cpu_baseline:
+        r = cpu_reference_run(args, n, spe, 2, seconds_cap=args.cpu_seconds)
+        cpu = {"value": r["value"], "unit": "samples/s", "cores": r["cores"],
+               "kind": "reference",
+               "sample": f"{r['steps']} steps x {B} samples (epoch 1) of the workload: "
+                         "reference permute_epoch/loc_distribution/balance/tail moves "
+                         "(oracle/_ref) + oracle C augment on all host threads, warm host "
+                         "cache of 4096 samples"}
+
+    totals = ld.epoch_totals()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": args.dtype, "data": "synthetic", "config": workload(args, n),
+                "clocks": clk.summary(),
+                "e2e": e2e,
+                "gpu_launches": int(launches1.value - launches0.value),
+                "roofline": {"bound": "hbm", "kernel": "augment_crop", "achieved": achieved,
+                             "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                             "traffic": traffic, "peak_source": peak_src,
+                             "algorithmic_bytes_per_launch": per_launch_bytes,
+                             "avg_launch_ms": aug_ms / aug_n if aug_n else None,
+                             "launches_timed": aug_n},
+                "kernel_ms": {k: (v[1] / v[0] if v[0] else None) for k, v in stats.items()},
+                "cpu_baseline": cpu,
+                "remote_per_epoch": {"loc_moved_samples": totals["moved"],
+                                     "loc_nvlink_bytes": totals["moved_nvlink"] * H * W * 3,
+                                     "reg_remote_samples": totals["reg_remote"],
+                                     "reg_remote_bytes": totals["reg_remote"] * H * W * 3,
+                                     "eq7_samples": d * (n - 1) / n}}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,325 @@
+// augment.cu -- K6 (crop) and K7 (bilinear resize): the fused preprocess.
+//
+// Replaces the reference's injected preprocess delay (PreprocessPacer,
+// proj/src/pipeline.cpp:87-108; real augmentation is a non-goal there,
+// SPEC.md:430,438).  Semantics are defined by oracle/locload_oracle.c
+// (lo_aug_params_for / lo_augment_one) and DESIGN.md section 4:
+//   stream SplitMix64(derive_seed(seed, epoch, id)):  y0 = bounded(H-ch+1),
+//   x0 = bounded(W-cw+1), flip = next() >> 63;
+//   out[c][y][x] = (float(src[y0+y][x0+x'][c]) - mean255[c]) * inv_std255[c]
+//   with x' = flip ? cw-1-x : x;  HWC u8 in, NCHW fp32 / bf16 (RNE) out.
+//
+// K6 (crop 224 from a fixed-size source) is HBM-bound: per sample it reads the
+// 224x224x3 window (150,528 B) and writes 602,112 B (fp32) or 301,056 B
+// (bf16).  One CTA = one sample x one 32-row band.  The band's source rows
+// (the crop window widened to 16-byte alignment, <= 688 B per row) are pulled
+// into shared memory with 128-bit non-allocating loads; each thread then emits
+// PX consecutive output pixels of all three planes as 128-bit streaming
+// stores, so every warp writes 512 contiguous bytes per plane row.
+#include "ll_internal.h"
+#include "ll_rng.cuh"
+
+#include <cuda_bf16.h>
+
+namespace ll {
+namespace {
+
+constexpr uint32_t kOut = 224;        // K6 output side (BASELINE configs)
+constexpr uint32_t kBand = 32;        // rows per CTA
+constexpr uint32_t kBands = kOut / kBand;
+constexpr uint32_t kRowSmem = 704;    // >= 672 + 2*15, multiple of 16
+constexpr uint32_t kThreads = 224;
+
+struct AugArgs {
+    SrcMap src;
+    uint32_t H, W;
+    uint64_t seed, epoch;
+    NormConst nc;
+    void* out;
+    uint64_t n;
+    uint32_t out_h, out_w;
+};
+
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+// Resolve sample k of a launch: id and source bytes.
+__device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* id,
+                                        const uint8_t** src) {
+    if (m.kind == 0) {
+        *id = m.ids[k];
+        *src = m.base + k * m.sample_bytes;
+        return;
+    }
+    const uint32_t* list = m.list_off ? m.list + *m.list_off : m.list;
+    const uint32_t kept = m.kept_dev ? *m.kept_dev : m.kept;
+    const uint64_t s = list[k];
+    *id = s;
+    if (k < kept) {
+        *src = m.shard + (s - m.shard_first) * m.sample_bytes;
+    } else if (m.peers) {
+        const uint32_t o = static_cast<uint32_t>(s * m.p / m.cached);
+        const uint64_t first = (static_cast<uint64_t>(o) * m.cached + m.p - 1) / m.p;
+        *src = m.peers[o] + (s - first) * m.sample_bytes;
+    } else {
+        *src = m.recv + (k - kept) * m.sample_bytes;
+    }
+}
+
+struct Params {
+    uint32_t y0, x0, ch, cw, flip;
+};
+
+__device__ __forceinline__ Params aug_params(uint64_t seed, uint64_t epoch, uint64_t id,
+                                             uint32_t H, uint32_t W, uint32_t out_h,
+                                             uint32_t out_w, int mode) {
+    Params q;
+    if (mode == LL_AUG_CROP) {
+        q.ch = out_h;
+        q.cw = out_w;
+    } else {
+        q.ch = q.cw = H < W ? H : W;
+    }
+    SplitMix r(derive_seed(seed, epoch, id));
+    q.y0 = static_cast<uint32_t>(r.bounded(static_cast<uint64_t>(H - q.ch) + 1));
+    q.x0 = static_cast<uint32_t>(r.bounded(static_cast<uint64_t>(W - q.cw) + 1));
+    q.flip = static_cast<uint32_t>(r.next() >> 63);
+    return q;
+}
+
+__device__ __forceinline__ float norm(uint32_t v, float mean, float inv) {
+    return __fmul_rn(__fsub_rn(static_cast<float>(v), mean), inv);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    const __nv_bfloat16 a = __float2bfloat16_rn(lo), b = __float2bfloat16_rn(hi);
+    return static_cast<uint32_t>(__bfloat16_as_ushort(a)) |
+           (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
+}
+
+// PX output pixels per thread: 4 (fp32, one float4 per plane) or 8 (bf16,
+// eight bf16 per plane).  kThreads/(224/PX) = PX rows per pass.
+template <bool BF16>
+__global__ void __launch_bounds__(kThreads) k_augment_crop(AugArgs a) {
+    constexpr uint32_t PX = BF16 ? 8 : 4;
+    constexpr uint32_t TPR = kOut / PX;  // threads per output row
+    __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
+    __shared__ const uint8_t* s_src;
+    __shared__ Params s_prm;
+
+    const uint64_t k = blockIdx.x / kBands;
+    const uint32_t band = blockIdx.x - static_cast<uint32_t>(k) * kBands;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        uint64_t id;
+        const uint8_t* src;
+        resolve(a.src, k, &id, &src);
+        s_src = src;
+        s_prm = aug_params(a.seed, a.epoch, id, a.H, a.W, kOut, kOut, LL_AUG_CROP);
+    }
+    __syncthreads();
+    const Params q = s_prm;
+    const uint8_t* src = s_src;
+    const uint32_t row_bytes = a.W * 3;
+    const uint32_t a0 = (3 * q.x0) & ~15u;
+    const uint32_t nch = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
+    const uint8_t* gbase = src + static_cast<uint64_t>(q.y0 + band * kBand) * row_bytes + a0;
+    for (uint32_t t = tid; t < kBand * nch; t += kThreads) {
+        const uint32_t r = t / nch, c = t - r * nch;
+        const uint4 v = ld_nc_v4(gbase + static_cast<uint64_t>(r) * row_bytes + 16 * c);
+        *reinterpret_cast<uint4*>(&rows[r][16 * c]) = v;
+    }
+    __syncthreads();
+
+    const uint32_t tr = tid / TPR, tq = tid - tr * TPR;
+    const uint64_t plane = static_cast<uint64_t>(kOut) * kOut;
+    const uint64_t obase = k * 3 * plane;
+    // byte offset (within the smem row) of output pixel tq*PX + u
+    int32_t b0, step;
+    if (q.flip) {
+        b0 = static_cast<int32_t>(3 * (q.x0 + kOut - 1 - tq * PX)) - static_cast<int32_t>(a0);
+        step = -3;
+    } else {
+        b0 = static_cast<int32_t>(3 * (q.x0 + tq * PX)) - static_cast<int32_t>(a0);
+        step = 3;
+    }
+#pragma unroll 1
+    for (uint32_t it = 0; it < kBand / PX; ++it) {
+        const uint32_t r = it * PX + tr;
+        const uint32_t oy = band * kBand + r;
+        const uint8_t* row = rows[r];
+        float v[3][PX];
+#pragma unroll
+        for (uint32_t u = 0; u < PX; ++u) {
+            const int32_t b = b0 + step * static_cast<int32_t>(u);
+#pragma unroll
+            for (uint32_t c = 0; c < 3; ++c) v[c][u] = norm(row[b + c], a.nc.mean255[c], a.nc.inv_std255[c]);
+        }
+        const uint64_t o = obase + static_cast<uint64_t>(oy) * kOut + tq * PX;
+#pragma unroll
+        for (uint32_t c = 0; c < 3; ++c) {
+            if constexpr (BF16) {
+                uint16_t* out = static_cast<uint16_t*>(a.out);
+                st_cs_v4(out + o + c * plane,
+                         make_uint4(pack_bf16(v[c][0], v[c][1]), pack_bf16(v[c][2], v[c][3]),
+                                    pack_bf16(v[c][4], v[c][5]), pack_bf16(v[c][6], v[c][7])));
+            } else {
+                float* out = static_cast<float*>(a.out);
+                st_cs_v4(out + o + c * plane,
+                         make_uint4(__float_as_uint(v[c][0]), __float_as_uint(v[c][1]),
+                                    __float_as_uint(v[c][2]), __float_as_uint(v[c][3])));
+            }
+        }
+    }
+}
+
+// K7: variable geometry, bilinear resize (half-pixel centres, edge clamp).
+// One CTA per (sample, output row); generic and straightforward (cfg5).
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_augment_resize(AugArgs a) {
+    const uint64_t k = blockIdx.x / a.out_h;
+    const uint32_t oy = blockIdx.x - static_cast<uint32_t>(k) * a.out_h;
+    __shared__ const uint8_t* s_src;
+    __shared__ Params s_prm;
+    if (threadIdx.x == 0) {
+        uint64_t id;
+        const uint8_t* src;
+        resolve(a.src, k, &id, &src);
+        s_src = src;
+        s_prm = aug_params(a.seed, a.epoch, id, a.H, a.W, a.out_h, a.out_w, LL_AUG_RESIZE);
+    }
+    __syncthreads();
+    const Params q = s_prm;
+    const uint8_t* src = s_src;
+    const float sy = __fdiv_rn(static_cast<float>(q.ch), static_cast<float>(a.out_h));
+    const float sx = __fdiv_rn(static_cast<float>(q.cw), static_cast<float>(a.out_w));
+    float fy = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(oy), 0.5f), sy), 0.5f);
+    if (fy < 0.f) fy = 0.f;
+    uint32_t ylo = static_cast<uint32_t>(fy);
+    if (ylo > q.ch - 1) ylo = q.ch - 1;
+    const uint32_t yhi = ylo + 1 < q.ch ? ylo + 1 : q.ch - 1;
+    const float wy = __fsub_rn(fy, static_cast<float>(ylo));
+    const uint8_t* r0 = src + static_cast<uint64_t>(q.y0 + ylo) * a.W * 3;
+    const uint8_t* r1 = src + static_cast<uint64_t>(q.y0 + yhi) * a.W * 3;
+    const uint64_t plane = static_cast<uint64_t>(a.out_h) * a.out_w;
+    for (uint32_t ox = threadIdx.x; ox < a.out_w; ox += blockDim.x) {
+        const uint32_t mx = q.flip ? a.out_w - 1 - ox : ox;
+        float fx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(mx), 0.5f), sx), 0.5f);
+        if (fx < 0.f) fx = 0.f;
+        uint32_t xlo = static_cast<uint32_t>(fx);
+        if (xlo > q.cw - 1) xlo = q.cw - 1;
+        const uint32_t xhi = xlo + 1 < q.cw ? xlo + 1 : q.cw - 1;
+        const float wx = __fsub_rn(fx, static_cast<float>(xlo));
+        const uint64_t pa = static_cast<uint64_t>(q.x0 + xlo) * 3, pb = static_cast<uint64_t>(q.x0 + xhi) * 3;
+#pragma unroll
+        for (uint32_t c = 0; c < 3; ++c) {
+            const float p00 = r0[pa + c], p01 = r0[pb + c], p10 = r1[pa + c], p11 = r1[pb + c];
+            const float top = __fadd_rn(p00, __fmul_rn(wx, __fsub_rn(p01, p00)));
+            const float bot = __fadd_rn(p10, __fmul_rn(wx, __fsub_rn(p11, p10)));
+            const float v = __fadd_rn(top, __fmul_rn(wy, __fsub_rn(bot, top)));
+            const float o = __fmul_rn(__fsub_rn(v, a.nc.mean255[c]), a.nc.inv_std255[c]);
+            const uint64_t idx = k * 3 * plane + c * plane + static_cast<uint64_t>(oy) * a.out_w + ox;
+            if constexpr (BF16)
+                static_cast<__nv_bfloat16*>(a.out)[idx] = __float2bfloat16_rn(o);
+            else
+                static_cast<float*>(a.out)[idx] = o;
+        }
+    }
+}
+
+__global__ void k_aug_params(uint64_t seed, uint64_t epoch, const uint64_t* __restrict__ ids,
+                             uint64_t n, uint32_t H, uint32_t W, uint32_t out_h, uint32_t out_w,
+                             int mode, uint32_t* __restrict__ out5) {
+    const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const Params q = aug_params(seed, epoch, ids[i], H, W, out_h, out_w, mode);
+    out5[5 * i + 0] = q.y0;
+    out5[5 * i + 1] = q.x0;
+    out5[5 * i + 2] = q.ch;
+    out5[5 * i + 3] = q.cw;
+    out5[5 * i + 4] = q.flip;
+}
+
+} // namespace
+
+NormConst norm_constants(const ll_augment_spec& s) {
+    NormConst c;
+    for (int i = 0; i < 3; ++i) {
+        c.mean255[i] = static_cast<float>(s.mean[i] * 255.0);
+        c.inv_std255[i] = static_cast<float>(1.0 / (s.std[i] * 255.0));
+    }
+    return c;
+}
+
+static void validate_spec(const ll_augment_spec& spec, uint32_t H, uint32_t W) {
+    require(spec.out_dtype == LL_OUT_F32 || spec.out_dtype == LL_OUT_BF16,
+            "augment: out_dtype must be fp32 or bf16");
+    if (spec.mode == LL_AUG_CROP) {
+        require(spec.out_h == kOut && spec.out_w == kOut, "augment: crop output must be 224x224");
+        require(H >= kOut && W >= kOut, "augment: source smaller than the crop");
+        require((3ull * W) % 16 == 0, "augment: source row bytes must be a multiple of 16");
+    } else {
+        require(spec.mode == LL_AUG_RESIZE, "augment: unknown mode");
+        require(spec.out_h >= 1 && spec.out_w >= 1 && H >= 1 && W >= 1,
+                "augment: empty geometry");
+    }
+}
+
+void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out) {
+    validate_spec(spec, height, width);
+    if (n == 0) return;
+    AugArgs a{};
+    a.src = src;
+    a.H = height;
+    a.W = width;
+    a.seed = seed;
+    a.epoch = epoch;
+    a.nc = norm_constants(spec);
+    a.out = d_out;
+    a.n = n;
+    a.out_h = spec.out_h;
+    a.out_w = spec.out_w;
+    const bool bf16 = spec.out_dtype == LL_OUT_BF16;
+    if (spec.mode == LL_AUG_CROP) {
+        const dim3 grid(static_cast<unsigned>(n * kBands));
+        launch(ctx, "augment_crop", [&] {
+            if (bf16)
+                k_augment_crop<true><<<grid, kThreads, 0, ctx->stream>>>(a);
+            else
+                k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);
+        });
+    } else {
+        const dim3 grid(static_cast<unsigned>(n * spec.out_h));
+        launch(ctx, "augment_resize", [&] {
+            if (bf16)
+                k_augment_resize<true><<<grid, 256, 0, ctx->stream>>>(a);
+            else
+                k_augment_resize<false><<<grid, 256, 0, ctx->stream>>>(a);
+        });
+    }
+}
+
+void augment_params_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed,
+                           uint64_t epoch, const uint64_t* d_ids, uint64_t n, uint32_t height,
+                           uint32_t width, uint32_t* d_params5) {
+    validate_spec(spec, height, width);
+    if (n == 0) return;
+    launch(ctx, "aug_params", [&] {
+        k_aug_params<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(
+            seed, epoch, d_ids, n, height, width, spec.out_h, spec.out_w, spec.mode, d_params5);
+    });
+}
+
+} // namespace ll

@@ -1,0 +1,180 @@
+// ll_internal.h -- context, errors and kernel-launch bookkeeping shared by the
+// translation units behind include/locload_b200.h.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "locload_b200.h"
+
+namespace ll {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void require(bool ok, const std::string& msg) {
+    if (!ok) fail(LL_ERR_INVALID, msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(LL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define LL_CUDA(x) ::ll::cuda_check((x), #x)
+
+// Device buffer with grow-only reallocation.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n) {
+        if (n <= bytes) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+        LL_CUDA(cudaMalloc(&ptr, n));
+        bytes = n;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+struct KernelTimes {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    uint64_t launches = 0;
+    double total_ms = 0;
+};
+
+} // namespace ll
+
+struct ll_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    bool timing = false;
+    std::map<std::string, ll::KernelTimes> times;
+    std::vector<cudaEvent_t> event_pool;
+    // named device scratch buffers (grow-only), e.g. "perm.J"
+    std::map<std::string, std::unique_ptr<ll::DevBuf>> scratch;
+    ll::DevBuf& buf(const std::string& name, size_t bytes) {
+        auto& p = scratch[name];
+        if (!p) p.reset(new ll::DevBuf());
+        p->reserve(bytes);
+        return *p;
+    }
+    cudaEvent_t take_event();
+};
+
+namespace ll {
+
+// Every kernel launch of the library goes through here: counts it, and when
+// timing is on brackets it with events on the context stream.
+template <typename F>
+void launch(ll_ctx* ctx, const char* name, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (ctx->timing) {
+        a = ctx->take_event();
+        b = ctx->take_event();
+        LL_CUDA(cudaEventRecord(a, ctx->stream));
+    }
+    f();
+    LL_CUDA(cudaGetLastError());
+    ctx->launches++;
+    if (ctx->timing) {
+        LL_CUDA(cudaEventRecord(b, ctx->stream));
+        ctx->times[name].pending.emplace_back(a, b);
+    }
+}
+
+void set_device(ll_ctx* ctx);
+
+// permute.cu: full permutation of [0,d) into d_order (u32), on ctx->stream.
+void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint32_t* d_order,
+                    const uint64_t* host_forced, uint64_t n_forced);
+
+// assign.cu
+constexpr uint32_t kMaxP = 64;
+struct PlanDev {
+    uint32_t* final_ids = nullptr;  // [steps][B]
+    uint32_t* off = nullptr;        // [steps][kMaxP+1]
+    uint32_t* kept = nullptr;       // [steps][kMaxP]
+    uint32_t* counts = nullptr;     // [steps][kMaxP]
+    ll_move* moves = nullptr;       // [steps][kMaxP]
+    uint32_t* n_moves = nullptr;    // [steps]
+    uint32_t* stats = nullptr;      // [steps][4]: moved, nvlink, uncached, reg_remote
+    uint32_t* scratch = nullptr;    // [steps][B]
+};
+struct PlanBufs {
+    DevBuf final_ids, off, kept, counts, moves, n_moves, stats, scratch;
+    PlanDev view() const;
+    void reserve(uint64_t steps, uint64_t B);
+};
+void assign_device(ll_ctx* ctx, const uint32_t* d_order, uint64_t steps, uint64_t B, uint32_t p,
+                   uint64_t cached, int scheme, const PlanDev& plan);
+void balance_device(ll_ctx* ctx, const int64_t* d_counts, const int64_t* d_targets, uint32_t p,
+                    uint64_t n, ll_move* d_moves, uint32_t* d_n);
+
+// shard.cu
+void generate_range_device(ll_ctx* ctx, uint8_t* dst, uint64_t first_id, uint64_t n,
+                           uint64_t sample_bytes, uint64_t data_seed);
+void generate_ids_device(ll_ctx* ctx, uint8_t* dst, const uint64_t* d_ids, uint64_t n,
+                         uint64_t sample_bytes, uint64_t data_seed);
+
+// augment.cu
+struct NormConst {
+    float mean255[3];
+    float inv_std255[3];
+};
+NormConst norm_constants(const ll_augment_spec& s);
+
+// Where output sample k of a launch reads its source bytes from.
+struct SrcMap {
+    int kind = 0;                      // 0 explicit, 1 plan
+    // explicit (tests): src = base + k * sample_bytes, id = ids[k]
+    const uint8_t* base = nullptr;
+    const uint64_t* ids = nullptr;
+    // plan: id = list[k]; k < kept -> own shard, else remote
+    const uint32_t* list = nullptr;
+    const uint32_t* list_off = nullptr;  // if set: list += *list_off (device)
+    uint32_t kept = 0;
+    const uint32_t* kept_dev = nullptr;  // if set: kept = *kept_dev (device)
+    const uint8_t* shard = nullptr;
+    uint64_t shard_first = 0;
+    const uint8_t* recv = nullptr;     // NCCL path: received samples in list order
+    const uint8_t* const* peers = nullptr;  // P2P path: every learner's shard
+    uint32_t p = 1;
+    uint64_t cached = 0;
+    uint64_t sample_bytes = 0;
+};
+void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out);
+void augment_params_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed,
+                           uint64_t epoch, const uint64_t* d_ids, uint64_t n, uint32_t height,
+                           uint32_t width, uint32_t* d_params5);
+
+// exchange.cu
+std::vector<ll_xfer> exchange_plan(const ll_move* moves, uint32_t n, const uint32_t* off,
+                                   uint32_t me);
+std::vector<ll_xfer> exchange_plan(const ll_move* moves, uint32_t n, const uint64_t* off,
+                                   uint32_t me);
+void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
+                 const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
+                 uint8_t* packbuf);
+
+} // namespace ll

@@ -1,0 +1,406 @@
+// loader.cu -- one learner of the locality-aware loader on one B200.
+//
+// Reference shape: Loader (proj/include/locload/pipeline.hpp:106-123,
+// pipeline.cpp:236-336) + SampleCache (pipeline.hpp:68-94), with the
+// locality-aware composition of equivalence.cpp:66-91.  What changes:
+//   * the cache is this learner's CacheDirectory block (sampling.cpp:19-25)
+//     held densely in HBM: sample s lives at shard + (s - first) * bytes --
+//     no hash map, no lock, no shared_ptr;
+//   * the epoch plan (permute_epoch + per-step assignment, schedule and tail
+//     moves) is computed on the device, identically on every learner, so
+//     learners agree on it without communicating (as in the reference's
+//     replicated directory, sampling.hpp:11-14);
+//   * per step, moved samples travel learner-to-learner (NCCL grouped
+//     send/recv over NVLink, or direct peer-HBM reads inside the augment
+//     kernel), then the fused augment writes the learner's NCHW batch;
+//   * delivery order is stream order; prefetch_depth is the output ring.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "ll_internal.h"
+
+namespace ll {
+void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
+void narrow_device(ll_ctx* ctx, const uint64_t* in, uint32_t* out, uint64_t n);
+uint32_t permute_rounds(ll_ctx* ctx);
+}
+
+#define LL_NCCL(x)                                                                        \
+    do {                                                                                  \
+        ncclResult_t r_ = (x);                                                            \
+        if (r_ != ncclSuccess)                                                            \
+            ::ll::fail(LL_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));     \
+    } while (0)
+
+struct ll_loader {
+    ll_ctx* ctx = nullptr;
+    ll_loader_config cfg{};
+    uint64_t S = 0;               // sample bytes
+    uint64_t cached = 0;          // CacheDirectory::cached_count
+    uint64_t first = 0, owned = 0;
+    uint64_t steps = 0;           // per epoch
+    uint64_t max_local = 0;
+    ll::DevBuf shard;
+    bool populated = false;
+    // epoch plan
+    ll::DevBuf order;
+    ll::PlanBufs plan;
+    int64_t plan_epoch = -1;
+    std::vector<ll_move> h_moves;
+    std::vector<uint32_t> h_off, h_kept, h_counts, h_nmoves, h_stats;
+    // single-step plan for the host-driven entry point
+    ll::DevBuf e2e_batch64, e2e_order;
+    ll::PlanBufs e2e_plan;
+    ll::DevBuf e2e_ids64;
+    // exchange
+    ncclComm_t comm = nullptr;
+    ll::DevBuf packbuf, recvbuf;
+    std::vector<void*> peer_open;  // opened IPC mappings (excluding self)
+    ll::DevBuf d_peers;
+    bool peers_ready = false;
+    // output ring
+    std::vector<std::unique_ptr<ll::DevBuf>> out;
+    uint32_t out_slot = 0;
+};
+
+namespace ll {
+namespace {
+
+uint64_t out_elem_bytes(const ll_loader_config& c) {
+    return c.augment.out_dtype == LL_OUT_BF16 ? 2 : 4;
+}
+
+void copy_tables(ll_loader* ld, const PlanBufs& plan, uint64_t steps) {
+    ll_ctx* ctx = ld->ctx;
+    ld->h_moves.resize(steps * kMaxP);
+    ld->h_off.resize(steps * (kMaxP + 1));
+    ld->h_kept.resize(steps * kMaxP);
+    ld->h_counts.resize(steps * kMaxP);
+    ld->h_nmoves.resize(steps);
+    ld->h_stats.resize(steps * 4);
+    auto d2h = [&](void* dst, const DevBuf& b, size_t n) {
+        LL_CUDA(cudaMemcpyAsync(dst, b.ptr, n, cudaMemcpyDeviceToHost, ctx->stream));
+    };
+    d2h(ld->h_moves.data(), plan.moves, sizeof(ll_move) * steps * kMaxP);
+    d2h(ld->h_off.data(), plan.off, sizeof(uint32_t) * steps * (kMaxP + 1));
+    d2h(ld->h_kept.data(), plan.kept, sizeof(uint32_t) * steps * kMaxP);
+    d2h(ld->h_counts.data(), plan.counts, sizeof(uint32_t) * steps * kMaxP);
+    d2h(ld->h_nmoves.data(), plan.n_moves, sizeof(uint32_t) * steps);
+    d2h(ld->h_stats.data(), plan.stats, sizeof(uint32_t) * steps * 4);
+    LL_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void ensure_out(ll_loader* ld) {
+    if (!ld->out.empty()) return;
+    const ll_loader_config& c = ld->cfg;
+    const uint64_t bytes =
+        ld->max_local * 3ull * c.augment.out_h * c.augment.out_w * out_elem_bytes(c);
+    for (uint32_t f = 0; f < std::max<uint32_t>(1, c.prefetch_depth); ++f) {
+        ld->out.emplace_back(new DevBuf());
+        ld->out.back()->reserve(bytes ? bytes : 16);
+    }
+}
+
+// Issue exchange + augment of one step whose plan tables are at (plan, step)
+// with host mirrors (h_*, index hs).
+void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
+              const ll_move* h_moves, const uint32_t* h_off, const uint32_t* h_kept,
+              uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info) {
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const uint32_t me = c.rank, p = c.learners;
+    const uint64_t B = c.batch_size;
+    const uint32_t* d_final_step = pd.final_ids + step * B;
+    const uint64_t n_local = h_off[me + 1] - h_off[me];
+    const uint64_t kept = h_kept[me];
+    uint64_t n_send = 0, n_recv = 0, nvl_recv = 0;
+    for (uint32_t m = 0; m < h_nmoves; ++m) {
+        if (h_moves[m].sender == me) n_send += h_moves[m].count;
+        if (h_moves[m].receiver == me) {
+            n_recv += h_moves[m].count;
+            nvl_recv += h_moves[m].nvlink;
+        }
+    }
+    SrcMap src;
+    src.kind = 1;
+    src.list = d_final_step + h_off[me];
+    src.kept = static_cast<uint32_t>(kept);
+    src.shard = ld->shard.as<uint8_t>();
+    src.shard_first = ld->first;
+    src.p = p;
+    src.cached = ld->cached;
+    src.sample_bytes = ld->S;
+    if (p > 1 && (n_send || n_recv)) {
+        if (c.exchange == LL_EXCHANGE_NCCL) {
+            require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
+            const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
+            ld->packbuf.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
+            ld->recvbuf.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
+            pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
+                        ld->packbuf.as<uint8_t>());
+            LL_NCCL(ncclGroupStart());
+            for (const ll_xfer& x : xs) {
+                if (x.is_send)
+                    LL_NCCL(ncclSend(ld->packbuf.as<uint8_t>() + x.buf_first * ld->S,
+                                     x.count * ld->S, ncclUint8, static_cast<int>(x.peer),
+                                     ld->comm, ctx->stream));
+                else
+                    LL_NCCL(ncclRecv(ld->recvbuf.as<uint8_t>() + x.buf_first * ld->S,
+                                     x.count * ld->S, ncclUint8, static_cast<int>(x.peer),
+                                     ld->comm, ctx->stream));
+            }
+            LL_NCCL(ncclGroupEnd());
+            src.recv = ld->recvbuf.as<uint8_t>();
+        } else if (c.exchange == LL_EXCHANGE_P2P) {
+            require(ld->peers_ready, "loader: P2P exchange needs peer shards (open/link)");
+            src.peers = ld->d_peers.as<const uint8_t*>();
+        } else {
+            fail(LL_ERR_INVALID, "loader: remote samples need an exchange (NCCL or P2P)");
+        }
+    }
+    ensure_out(ld);
+    void* out = ld->out[ld->out_slot]->ptr;
+    ld->out_slot = (ld->out_slot + 1) % ld->out.size();
+    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, c.height, c.width, out);
+    if (info) {
+        info->epoch = epoch;
+        info->step = step;
+        info->n_local = n_local;
+        info->kept = kept;
+        info->received = n_recv;
+        info->moved_total = h_stats[0];
+        info->nvlink_bytes = nvl_recv * ld->S;
+        info->uncached = h_stats[2];
+        info->reg_remote = h_stats[3] == 0xFFFFFFFFu ? UINT64_MAX : h_stats[3];
+        info->device_out = reinterpret_cast<uintptr_t>(out);
+        info->device_ids = reinterpret_cast<uintptr_t>(d_final_step + h_off[me]);
+    }
+}
+
+} // namespace
+
+void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
+    require(cfg != nullptr, "Loader: null config");
+    const ll_loader_config& c = *cfg;
+    // pipeline.cpp:237-241
+    require(c.batch_size >= 1 && c.prefetch_depth >= 1,
+            "Loader: workers, parallelism, prefetch and batch size must all be >= 1");
+    require(c.learners >= 1, "CacheDirectory: learner count must be >= 1");
+    require(c.alpha > 0.0 && c.alpha <= 1.0, "CacheDirectory: cached fraction must be in (0, 1]");
+    require(c.d >= 1, "permute_epoch: dataset must contain at least one sample");
+    require(c.batch_size <= c.d, "batches: batch size must be in [1, dataset size]");
+    require(c.learners <= kMaxP, "Loader: at most 64 learners per box");
+    require(c.rank < c.learners, "Loader: rank out of range");
+    require(c.d < 0xFFFFFFFFull, "Loader: dataset size must be < 2^32 - 1 on the device");
+    require(c.height >= 1 && c.width >= 1, "Loader: empty sample geometry");
+    require(c.scheme >= LL_SCHEME_REGULAR && c.scheme <= LL_SCHEME_LOCALITY_BALANCED,
+            "Loader: unknown scheme");
+    if (c.scheme == LL_SCHEME_REGULAR)
+        require(c.batch_size % c.learners == 0,
+                "reg_slice: learner count must divide the batch size");
+    auto ld = std::make_unique<ll_loader>();
+    ld->ctx = ctx;
+    ld->cfg = c;
+    ld->S = static_cast<uint64_t>(c.height) * c.width * 3;
+    ld->cached = static_cast<uint64_t>(c.alpha * static_cast<double>(c.d));  // sampling.cpp:15
+    if (ld->cached > c.d) ld->cached = c.d;
+    require(ld->cached >= 1, "Loader: alpha * d must cache at least one sample");
+    require(ld->cached == c.d, "Loader: alpha < 1 needs the storage tier (not built yet)");
+    const uint64_t p = c.learners, j = c.rank;
+    ld->first = (j * ld->cached + p - 1) / p;
+    ld->owned = ((j + 1) * ld->cached + p - 1) / p - ld->first;
+    ld->steps = c.d / c.batch_size;
+    ld->max_local = c.scheme == LL_SCHEME_LOCALITY ? c.batch_size
+                                                   : (c.batch_size + p - 1) / p;
+    set_device(ctx);
+    ld->shard.reserve(std::max<uint64_t>(ld->owned * ld->S, 16));
+    ld->order.reserve(sizeof(uint32_t) * c.d);
+    ld->plan.reserve(ld->steps, c.batch_size);
+    *out = ld.release();
+}
+
+void loader_destroy(ll_loader* ld) {
+    if (!ld) return;
+    cudaSetDevice(ld->ctx->device);
+    for (void* p : ld->peer_open) cudaIpcCloseMemHandle(p);
+    if (ld->comm) ncclCommDestroy(ld->comm);
+    delete ld;
+}
+
+void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
+    set_device(ld->ctx);
+    ncclUniqueId id;
+    static_assert(sizeof(id) == 128, "ncclUniqueId size");
+    std::memcpy(&id, id128, sizeof(id));
+    LL_NCCL(ncclCommInitRank(&ld->comm, static_cast<int>(ld->cfg.learners), id,
+                             static_cast<int>(ld->cfg.rank)));
+}
+
+void loader_ipc_handle(ll_loader* ld, uint8_t* out64) {
+    set_device(ld->ctx);
+    cudaIpcMemHandle_t h;
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+    LL_CUDA(cudaIpcGetMemHandle(&h, ld->shard.ptr));
+    std::memcpy(out64, &h, sizeof(h));
+}
+
+void loader_open_peers(ll_loader* ld, const uint8_t* handles) {
+    set_device(ld->ctx);
+    const uint32_t p = ld->cfg.learners;
+    std::vector<const uint8_t*> ptrs(p);
+    for (uint32_t j = 0; j < p; ++j) {
+        if (j == ld->cfg.rank) {
+            ptrs[j] = ld->shard.as<uint8_t>();
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + 64ull * j, sizeof(h));
+        void* ptr = nullptr;
+        LL_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        ld->peer_open.push_back(ptr);
+        ptrs[j] = static_cast<const uint8_t*>(ptr);
+    }
+    ld->d_peers.reserve(sizeof(void*) * p);
+    LL_CUDA(cudaMemcpy(ld->d_peers.ptr, ptrs.data(), sizeof(void*) * p, cudaMemcpyHostToDevice));
+    ld->peers_ready = true;
+}
+
+void loader_link_peers(ll_loader* const* lds, uint32_t n) {
+    require(n >= 1, "link_peers: no loaders");
+    const uint32_t p = lds[0]->cfg.learners;
+    require(n == p, "link_peers: need one loader per learner");
+    std::vector<const uint8_t*> ptrs(p, nullptr);
+    for (uint32_t i = 0; i < n; ++i) {
+        require(lds[i]->cfg.learners == p, "link_peers: learner counts differ");
+        ptrs[lds[i]->cfg.rank] = lds[i]->shard.as<uint8_t>();
+    }
+    for (uint32_t j = 0; j < p; ++j) require(ptrs[j] != nullptr, "link_peers: missing rank");
+    for (uint32_t i = 0; i < n; ++i) {
+        set_device(lds[i]->ctx);
+        lds[i]->d_peers.reserve(sizeof(void*) * p);
+        LL_CUDA(cudaMemcpy(lds[i]->d_peers.ptr, ptrs.data(), sizeof(void*) * p,
+                           cudaMemcpyHostToDevice));
+        lds[i]->peers_ready = true;
+    }
+}
+
+void loader_populate(ll_loader* ld) {
+    set_device(ld->ctx);
+    generate_range_device(ld->ctx, ld->shard.as<uint8_t>(), ld->first, ld->owned, ld->S,
+                          ld->cfg.data_seed);
+    LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));
+    ld->populated = true;
+}
+
+void loader_populate_from_host(ll_loader* ld, const uint8_t* host) {
+    set_device(ld->ctx);
+    LL_CUDA(cudaMemcpyAsync(ld->shard.ptr, host, ld->owned * ld->S, cudaMemcpyHostToDevice,
+                            ld->ctx->stream));
+    LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));
+    ld->populated = true;
+}
+
+void loader_shard_range(ll_loader* ld, uint64_t* first, uint64_t* count) {
+    *first = ld->first;
+    *count = ld->owned;
+}
+
+uint64_t loader_steps(ll_loader* ld) { return ld->steps; }
+
+void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
+    set_device(ld->ctx);
+    const ll_loader_config& c = ld->cfg;
+    permute_device(ld->ctx, c.seed, epoch, static_cast<uint32_t>(c.d), ld->order.as<uint32_t>(),
+                   nullptr, 0);
+    assign_device(ld->ctx, ld->order.as<uint32_t>(), ld->steps, c.batch_size, c.learners,
+                  ld->cached, c.scheme, ld->plan.view());
+    copy_tables(ld, ld->plan, ld->steps);
+    ld->plan_epoch = static_cast<int64_t>(epoch);
+}
+
+void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* info) {
+    require(ld->populated, "Loader: shard not populated");
+    require(step < ld->steps, "Loader: step out of range");
+    if (ld->plan_epoch != static_cast<int64_t>(epoch)) loader_plan_epoch(ld, epoch);
+    set_device(ld->ctx);
+    run_step(ld, epoch, ld->plan.view(), step, &ld->h_moves[step * kMaxP],
+             &ld->h_off[step * (kMaxP + 1)], &ld->h_kept[step * kMaxP], ld->h_nmoves[step],
+             &ld->h_stats[step * 4], info);
+}
+
+void loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch,
+                      uint64_t* host_local_ids, ll_step_info* info) {
+    require(ld->populated, "Loader: shard not populated");
+    set_device(ld->ctx);
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const uint64_t B = c.batch_size;
+    ld->e2e_batch64.reserve(sizeof(uint64_t) * B);
+    ld->e2e_order.reserve(sizeof(uint32_t) * B);
+    ld->e2e_plan.reserve(1, B);
+    LL_CUDA(cudaMemcpyAsync(ld->e2e_batch64.ptr, host_batch, sizeof(uint64_t) * B,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    narrow_device(ctx, ld->e2e_batch64.as<uint64_t>(), ld->e2e_order.as<uint32_t>(), B);
+    assign_device(ctx, ld->e2e_order.as<uint32_t>(), 1, B, c.learners, ld->cached, c.scheme,
+                  ld->e2e_plan.view());
+    // the host needs this step's counts to size the grid and the messages
+    ll_move h_moves[kMaxP];
+    uint32_t h_off[kMaxP + 1], h_kept[kMaxP], h_n = 0, h_stats[4];
+    LL_CUDA(cudaMemcpyAsync(h_moves, ld->e2e_plan.moves.ptr, sizeof(h_moves),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    LL_CUDA(cudaMemcpyAsync(h_off, ld->e2e_plan.off.ptr, sizeof(h_off), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    LL_CUDA(cudaMemcpyAsync(h_kept, ld->e2e_plan.kept.ptr, sizeof(h_kept),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    LL_CUDA(cudaMemcpyAsync(&h_n, ld->e2e_plan.n_moves.ptr, sizeof(h_n), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    LL_CUDA(cudaMemcpyAsync(h_stats, ld->e2e_plan.stats.ptr, sizeof(h_stats),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    LL_CUDA(cudaStreamSynchronize(ctx->stream));
+    ll_step_info local{};
+    run_step(ld, epoch, ld->e2e_plan.view(), 0, h_moves, h_off, h_kept, h_n, h_stats, &local);
+    local.step = step;
+    const uint64_t n_local = local.n_local;
+    ld->e2e_ids64.reserve(sizeof(uint64_t) * std::max<uint64_t>(n_local, 1));
+    widen_device(ctx, ld->e2e_plan.final_ids.as<uint32_t>() + h_off[c.rank],
+                 ld->e2e_ids64.as<uint64_t>(), n_local);
+    LL_CUDA(cudaMemcpyAsync(host_local_ids, ld->e2e_ids64.ptr, sizeof(uint64_t) * n_local,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    LL_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (info) *info = local;
+}
+
+void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
+                      uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves) {
+    require(ld->plan_epoch >= 0, "Loader: no epoch planned");
+    require(step < ld->steps, "Loader: step out of range");
+    set_device(ld->ctx);
+    const uint64_t B = ld->cfg.batch_size;
+    const uint32_t p = ld->cfg.learners;
+    std::vector<uint32_t> ids(B);
+    LL_CUDA(cudaMemcpy(ids.data(), ld->plan.final_ids.as<uint32_t>() + step * B,
+                       sizeof(uint32_t) * B, cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < B; ++i) final_ids[i] = ids[i];
+    for (uint32_t j = 0; j <= p; ++j) final_off[j] = ld->h_off[step * (kMaxP + 1) + j];
+    for (uint32_t j = 0; j < p; ++j) {
+        kept[j] = ld->h_kept[step * kMaxP + j];
+        counts[j] = ld->h_counts[step * kMaxP + j];
+    }
+    *n_moves = ld->h_nmoves[step];
+    for (uint32_t m = 0; m < *n_moves; ++m) moves[m] = ld->h_moves[step * kMaxP + m];
+}
+
+void loader_epoch_totals(ll_loader* ld, uint64_t* out4) {
+    require(ld->plan_epoch >= 0, "Loader: no epoch planned");
+    for (int k = 0; k < 4; ++k) out4[k] = 0;
+    for (uint64_t s = 0; s < ld->steps; ++s)
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t v = ld->h_stats[s * 4 + k];
+            out4[k] += (v == 0xFFFFFFFFu) ? 0 : v;
+        }
+}
+
+} // namespace ll

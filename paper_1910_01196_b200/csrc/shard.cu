@@ -1,0 +1,76 @@
+// shard.cu -- K1: synthesize dataset samples straight into HBM.
+//
+// Byte formula of generate_dataset, proj/src/pipeline.cpp:221-226: byte i of
+// sample `id` is byte (i mod 8), little-endian, of draw i/8 of
+// SplitMix64(derive_seed(seed, id)).  Because the stream is counter based,
+// every 16-byte chunk (draws 2c, 2c+1) is independent: one thread writes one
+// 128-bit chunk with a streaming store.  Write-bound: HBM roofline.
+#include "ll_internal.h"
+#include "ll_rng.cuh"
+
+namespace ll {
+namespace {
+
+__device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ void gen_chunk(uint8_t* dst_sample, uint64_t key, uint64_t c,
+                                          uint64_t sample_bytes, bool vec) {
+    const uint64_t w0 = draw_at(key, 2 * c), w1 = draw_at(key, 2 * c + 1);
+    const uint64_t byte0 = 16 * c;
+    if (vec && byte0 + 16 <= sample_bytes) {
+        st_cs_v4(dst_sample + byte0,
+                 make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32),
+                            static_cast<uint32_t>(w1), static_cast<uint32_t>(w1 >> 32)));
+    } else {
+        for (uint64_t b = byte0; b < sample_bytes; ++b) {
+            const uint64_t w = (b - byte0) < 8 ? w0 : w1;
+            dst_sample[b] = static_cast<uint8_t>(w >> (((b - byte0) & 7) * 8));
+        }
+    }
+}
+
+// dst is [n][sample_bytes]; sample t has id first_id + t (or ids[t]).
+__global__ void k_generate(uint8_t* __restrict__ dst, uint64_t first_id,
+                           const uint64_t* __restrict__ ids, uint64_t n, uint64_t sample_bytes,
+                           uint64_t chunks_per_sample, uint64_t data_seed, bool vec) {
+    const uint64_t total = n * chunks_per_sample;
+    for (uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; g < total;
+         g += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t t = g / chunks_per_sample, c = g - t * chunks_per_sample;
+        const uint64_t id = ids ? ids[t] : first_id + t;
+        gen_chunk(dst + t * sample_bytes, derive_seed(data_seed, id), c, sample_bytes, vec);
+    }
+}
+
+void run(ll_ctx* ctx, uint8_t* dst, uint64_t first_id, const uint64_t* ids, uint64_t n,
+         uint64_t sample_bytes, uint64_t data_seed) {
+    if (n == 0 || sample_bytes == 0) return;
+    const uint64_t cps = (sample_bytes + 15) / 16;
+    const uint64_t total = n * cps;
+    const uint64_t cap = static_cast<uint64_t>(ctx->sm_count) * 8;  // 8 x 256-thread CTAs / SM
+    const uint64_t want = (total + 255) / 256;
+    const unsigned grid = static_cast<unsigned>(want < cap ? want : cap);
+    const bool vec = (reinterpret_cast<uintptr_t>(dst) % 16 == 0) && (sample_bytes % 16 == 0);
+    launch(ctx, "generate", [&] {
+        k_generate<<<grid, 256, 0, ctx->stream>>>(dst, first_id, ids, n, sample_bytes, cps,
+                                                  data_seed, vec);
+    });
+}
+
+} // namespace
+
+void generate_range_device(ll_ctx* ctx, uint8_t* dst, uint64_t first_id, uint64_t n,
+                           uint64_t sample_bytes, uint64_t data_seed) {
+    run(ctx, dst, first_id, nullptr, n, sample_bytes, data_seed);
+}
+
+void generate_ids_device(ll_ctx* ctx, uint8_t* dst, const uint64_t* d_ids, uint64_t n,
+                         uint64_t sample_bytes, uint64_t data_seed) {
+    run(ctx, dst, 0, d_ids, n, sample_bytes, data_seed);
+}
+
+} // namespace ll

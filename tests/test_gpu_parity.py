@@ -1,0 +1,452 @@
+"""CUDA path vs the oracle / the reference's golden vectors, through the C-ABI.
+
+Bars (north_star): permutation, per-learner assignment and remote-fetch lists
+bit-exact; augmented tensors within 1e-5 abs (fp32) / 1 ulp (bf16) after
+normalisation -- the kernels are in fact bit-exact with the oracle and the
+tests assert that too.  Mirrors the reference suites test_core.cpp,
+test_sampling.cpp, test_balance.cpp, test_pipeline.cpp (cited per test).
+"""
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1910_01196_b200 as ll
+from paper_1910_01196_b200 import _capi
+from paper_1910_01196_b200.loader import AugmentConfig, DeviceLoader, LoaderConfig
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+
+
+def bf16_ulps(a: np.ndarray, b: np.ndarray) -> int:
+    """max distance in bf16 ulps between two arrays of bf16 bit patterns"""
+    def key(x):
+        x = x.astype(np.int32)
+        return np.where(x & 0x8000, 0x8000 - (x & 0x7FFF), x + 0x8000)
+    return int(np.abs(key(a) - key(b)).max()) if a.size else 0
+
+
+# ------------------------------------------------------------- core (K2+K3)
+def test_permute_matches_reference_golden(golden):
+    for c in golden["permutations"]:
+        o = ll.permute_epoch(c["seed"], c["epoch"], c["d"]).order
+        if "order" in c:
+            assert o.tolist() == c["order"], (c["seed"], c["epoch"], c["d"])
+        else:
+            assert o[:64].tolist() == c["head"]
+            assert hashlib.sha256(o.tobytes()).hexdigest() == c["sha256"], c["d"]
+
+
+def test_permute_random_vs_oracle():
+    rng = np.random.default_rng(11)
+    for d in [1, 2, 3, 31, 32, 33, 511, 512, 513, 16383, 16384, 16385, 65537, 200003]:
+        s, e = int(rng.integers(0, 2 ** 63)), int(rng.integers(0, 1000))
+        assert np.array_equal(ll.permute_epoch(s, e, d).order, oracle.permute_epoch(s, e, d)), d
+
+
+@pytest.mark.parametrize("forced", [[0], [5], [999], [3, 4, 5], [10, 500, 998], [998, 999],
+                                    [1, 1000, 1500]])
+def test_permute_forced_rejections_vs_oracle(forced):
+    """The Lemire retry path (rng.hpp:41-50): draw indices forced to reject."""
+    d = 1000
+    f = np.ascontiguousarray(sorted(forced), dtype=np.uint64)
+    out = np.empty(d, np.uint64)
+    import ctypes as C
+    _capi.check(_capi.lib().ll_permute_epoch_forced(ll.locload.context(), 5, 1, d,
+                                                    _capi.ptr(f, C.c_uint64), len(f),
+                                                    _capi.ptr(out, C.c_uint64)))
+    assert np.array_equal(out, oracle.permute_epoch(5, 1, d, forced=forced))
+
+
+def test_permute_large_forced_vs_oracle():
+    import ctypes as C
+    d = 300000
+    forced = [7, 123456, 123457, 299990]
+    f = np.ascontiguousarray(forced, dtype=np.uint64)
+    out = np.empty(d, np.uint64)
+    _capi.check(_capi.lib().ll_permute_epoch_forced(ll.locload.context(), 9, 0, d,
+                                                    _capi.ptr(f, C.c_uint64), len(f),
+                                                    _capi.ptr(out, C.c_uint64)))
+    assert np.array_equal(out, oracle.permute_epoch(9, 0, d, forced=forced))
+
+
+def test_single_sample_and_errors():
+    assert ll.permute_epoch(7, 0, 1).order.tolist() == [0]  # test_core.cpp:12-15
+    with pytest.raises(ValueError, match="permute_epoch: dataset must contain"):
+        ll.permute_epoch(7, 0, 0)  # test_core.cpp:41-44
+    with pytest.raises(ValueError, match="permutation_prefix"):
+        ll.permutation_prefix(7, 0, 0, 0)
+
+
+def test_determinism_and_bijection():
+    """test_core.cpp:17-39"""
+    a, b = ll.permute_epoch(7, 0, 12).order, ll.permute_epoch(7, 0, 12).order
+    assert np.array_equal(a, b)
+    assert not np.array_equal(a, ll.permute_epoch(7, 1, 12).order)
+    assert not np.array_equal(a, ll.permute_epoch(8, 0, 12).order)
+    for d in [1, 2, 13, 1000, 10000]:
+        o = ll.permute_epoch(123, 4, d).order
+        assert sorted(o.tolist()) == list(range(d))
+
+
+def test_positions_uniform_across_seeds():
+    """test_core.cpp:49-73: chi-square over 20 bins, 1000 seeds, crit 43.82."""
+    d, bins, seeds = 10000, 20, 1000
+    pos = {0: [], 1234: [], 9999: []}
+    for s in range(seeds):
+        o = ll.permute_epoch(s, 0, d).order
+        inv = np.empty(d, np.int64)
+        inv[o.astype(np.int64)] = np.arange(d)
+        for t in pos:
+            pos[t].append(inv[t])
+    for t, ps in pos.items():
+        h = np.bincount(np.array(ps) * bins // d, minlength=bins)
+        exp = seeds / bins
+        assert ((h - exp) ** 2 / exp).sum() < 43.82, t
+
+
+def test_prefix_matches_dense():
+    """test_core.cpp:75-85"""
+    d = 5000
+    full = ll.permute_epoch(99, 3, d).order
+    for k in [0, 1, 64, 4096, d]:
+        assert np.array_equal(ll.permutation_prefix(99, 3, d, k), full[:k])
+    with pytest.raises(ValueError):
+        ll.permutation_prefix(99, 3, d, d + 1)
+
+
+def test_batches():
+    """test_core.cpp:87-122"""
+    perm = ll.permute_epoch(7, 0, 10)
+    bs = ll.batches(perm, 4)
+    assert len(bs) == 2 and all(len(b.samples) == 4 for b in bs)
+    perm = ll.permute_epoch(11, 2, 1024)
+    bs = ll.batches(perm, 64)
+    assert len(bs) == 16
+    assert sorted(np.concatenate([b.samples for b in bs]).tolist()) == list(range(1024))
+    with pytest.raises(ValueError):
+        ll.batches(perm, 0)
+    with pytest.raises(ValueError):
+        ll.batches(perm, 1025)
+
+
+def test_permute_rounds_reported():
+    ll.permute_epoch(42, 0, 1280000)
+    import ctypes as C
+    r = C.c_uint32()
+    _capi.check(_capi.lib().ll_last_permute_rounds(ll.locload.context(), C.byref(r)))
+    assert 10 < r.value < 200
+
+
+# ---------------------------------------------------- sampling + balance (K4)
+def test_assign_matches_reference_golden(golden):
+    for c in golden["assign_balanced"]:
+        a = ll.assign_batch(c["batch"], c["d"], c["p"], 1.0, _capi.SCHEME_LOCALITY_BALANCED)
+        assert a.final_ids.tolist() == c["lists"], (c["d"], c["p"], c["B"], c["step"])
+        assert a.final_off.tolist() == c["off"]
+        assert [m[:3] for m in a.moves] == [tuple(m) for m in c["moves"]]
+
+
+def test_assign_vs_oracle_random_all_schemes():
+    rng = np.random.default_rng(5)
+    for _ in range(150):
+        p = int(rng.integers(1, 65))
+        d = int(rng.integers(max(p, 64), 20000))
+        B = int(rng.integers(1, min(d, 5000)))
+        alpha = float(rng.choice([1.0, 1.0, 0.5, 0.25, 0.73, 0.01]))
+        batch = rng.choice(d, B, replace=False).astype(np.uint64)
+        cached = oracle.cached_count(d, alpha)
+        for scheme in [_capi.SCHEME_LOCALITY, _capi.SCHEME_LOCALITY_BALANCED]:
+            a = ll.assign_batch(batch, d, p, alpha, scheme)
+            r = oracle.assign_step(batch, p, cached, scheme)
+            assert np.array_equal(a.final_ids, r["final_ids"])
+            assert np.array_equal(a.final_off, r["final_off"])
+            assert np.array_equal(a.kept, r["kept"])
+            assert np.array_equal(a.counts, r["counts"])
+            assert [m[:5] for m in a.moves] == [tuple(int(x) for x in m) for m in r["moves"]]
+            # NVLink count per move = cached samples in the moved run
+            for m in a.moves:
+                run = a.final_ids[a.final_off[m[1]] + m[4]:a.final_off[m[1]] + m[4] + m[2]]
+                assert m[5] == int((run < cached).sum())
+        if B % p == 0:
+            a = ll.assign_batch(batch, d, p, alpha, _capi.SCHEME_REGULAR)
+            assert np.array_equal(a.final_ids, batch)
+            owners = np.array([oracle.lib().lo_owner(int(s), p, cached) for s in batch])
+            reg_learner = np.arange(B) // (B // p)
+            assert a.stats[3] == int(((owners != reg_learner) & (owners < p)).sum())
+
+
+def test_loc_distribution_reference_cases():
+    """test_sampling.cpp:85-123, 195-203"""
+    batch = ll.GlobalBatch(0, np.array([0, 13, 25, 14, 26, 15, 27, 16, 28, 17, 1, 18], np.uint64))
+    dist = ll.loc_distribution(batch, ll.CacheDirectory(36, 3, 1.0))
+    assert dist.counts == [2, 6, 4] and len(dist.uncached) == 0
+    assert dist.assignments[0].samples.tolist() == [0, 1]
+    assert dist.assignments[1].samples.tolist() == [13, 14, 15, 16, 17, 18]
+    assert dist.assignments[2].samples.tolist() == [25, 26, 27, 28]
+    b2 = ll.GlobalBatch(0, np.array([0, 6, 7, 8, 9, 5], np.uint64))
+    dist = ll.loc_distribution(b2, ll.CacheDirectory(12, 3, 0.5))
+    assert dist.counts == [1, 0, 1]
+    assert dist.uncached.tolist() == [6, 7, 8, 9]
+    assert ll.counts_with_uncached(dist, 3) == [3, 1, 2]
+    rb = ll.GlobalBatch(0, np.array([5, 9, 1, 7, 0, 3, 11, 2, 8, 10, 4, 6], np.uint64))
+    assert ll.reg_slice(rb, 3, 0).samples.tolist() == [5, 9, 1, 7]
+    assert ll.reg_slice(rb, 1, 0).samples.tolist() == rb.samples.tolist()
+    with pytest.raises(ValueError, match="reg_slice: learner count must divide"):
+        ll.reg_slice(rb, 5, 0)
+    with pytest.raises(ValueError, match="reg_slice: learner rank out of range"):
+        ll.reg_slice(rb, 3, 3)
+
+
+def test_partial_cache_vs_reference_golden(golden):
+    for c in golden["loc_distribution_partial"]:
+        dist = ll.loc_distribution(ll.GlobalBatch(0, np.array(c["batch"], np.uint64)),
+                                   ll.CacheDirectory(c["d"], c["p"], c["alpha"]))
+        assert dist.counts == c["counts"]
+        assert dist.uncached.tolist() == c["uncached"]
+        assert [a.samples.tolist() for a in dist.assignments] == c["lists"]
+        assert ll.counts_with_uncached(dist, c["p"]) == c["cwu"]
+
+
+def test_balance_matches_reference_golden(golden):
+    by_p = {}
+    for c in golden["balance"]:
+        by_p.setdefault(len(c["counts"]), []).append(c)
+    for p, cases in by_p.items():
+        ivs = [ll.ImbalanceVector(c["counts"], c["targets"]) for c in cases]
+        got = ll.balance_many(ivs)
+        for c, s in zip(cases, got):
+            assert [(m.sender, m.receiver, m.count) for m in s.moves] == \
+                [tuple(m) for m in c["moves"]]
+
+
+def test_balance_reference_examples_and_properties():
+    """test_balance.cpp:55-101"""
+    def mv(c, t):
+        return [(m.sender, m.receiver, m.count)
+                for m in ll.balance(ll.ImbalanceVector(c, t)).moves]
+    assert mv([2, 6, 4], [4, 4, 4]) == [(1, 0, 2)]
+    assert mv([10, 0, 2], [4, 4, 4]) == [(0, 1, 4), (0, 2, 2)]
+    assert mv([6, 6, 2, 2], [4, 4, 4, 4]) == [(0, 2, 2), (1, 3, 2)]
+    assert mv([4, 4, 4], [4, 4, 4]) == [] and mv([], []) == []
+    with pytest.raises(ValueError):
+        mv([1, 2], [4, 4])
+    with pytest.raises(ValueError):
+        mv([1, 2, 3], [3, 3])
+    rng = np.random.default_rng(404)
+    for p in range(1, 65):
+        ivs = []
+        for _ in range(32):
+            b = int(rng.integers(0, 8 * p + 1))
+            cnt = np.bincount(rng.integers(0, p, b), minlength=p).tolist()
+            ivs.append(ll.ImbalanceVector(cnt, ll.targets(b, p)))
+        for iv, s in zip(ivs, ll.balance_many(ivs)):
+            net = [0] * p
+            for m in s.moves:
+                assert m.count >= 1 and m.sender != m.receiver
+                net[m.sender] -= m.count
+                net[m.receiver] += m.count
+            assert net == [t - c for c, t in zip(iv.counts, iv.targets)]
+            assert len(s.moves) <= max(p - 1, 0)
+
+
+# ------------------------------------------------------------- dataset (K1)
+def test_generated_bytes_match_reference_golden(golden):
+    import ctypes as C
+    for c in golden["samples"]:
+        ids = np.array([c["id"]], np.uint64)
+        out = np.empty(c["bytes"], np.uint8)
+        _capi.check(_capi.lib().ll_generate_samples(ll.locload.context(), c["seed"],
+                                                    _capi.ptr(ids, C.c_uint64), 1, c["bytes"],
+                                                    _capi.ptr(out, C.c_uint8)))
+        assert out[:32].tobytes().hex() == c["head"]
+        assert hashlib.sha256(out.tobytes()).hexdigest() == c["sha256"]
+
+
+# ------------------------------------------------------------- augment (K6/K7)
+def device_augment(src, ids, H, W, seed, epoch, mode="crop", dtype="fp32", oh=224, ow=224):
+    import ctypes as C
+    spec = AugmentConfig(mode=mode, out_dtype=dtype, out_h=oh, out_w=ow).to_c()
+    n = len(ids)
+    out = np.empty((n, 3, oh, ow), np.float32 if dtype == "fp32" else np.uint16)
+    s = np.ascontiguousarray(src, dtype=np.uint8)
+    i = np.ascontiguousarray(ids, dtype=np.uint64)
+    _capi.check(_capi.lib().ll_augment(ll.locload.context(), C.byref(spec), seed, epoch,
+                                       _capi.ptr(s, C.c_uint8), _capi.ptr(i, C.c_uint64), n, H,
+                                       W, out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_crop_augment_vs_oracle(dtype):
+    rng = np.random.default_rng(1)
+    ids = rng.choice(10 ** 6, 40, replace=False).astype(np.uint64)
+    src = oracle.gen_samples(42, ids, 256 * 256 * 3)
+    got = device_augment(src, ids, 256, 256, 42, 1, dtype=dtype)
+    for k, sid in enumerate(ids):
+        want = oracle.augment(src[k].reshape(256, 256, 3), int(sid), 42, 1, bf16=dtype == "bf16")
+        if dtype == "fp32":
+            assert np.abs(got[k] - want).max() <= FP32_TOL
+        else:
+            assert bf16_ulps(got[k], want) <= 1
+        assert np.array_equal(got[k], want)  # bit-exact in practice
+
+
+def test_crop_augment_non_square_source():
+    ids = np.arange(9, dtype=np.uint64)
+    H, W = 240, 320
+    src = oracle.gen_samples(3, ids, H * W * 3)
+    got = device_augment(src, ids, H, W, 5, 0)
+    for k in range(len(ids)):
+        assert np.array_equal(got[k], oracle.augment(src[k].reshape(H, W, 3), k, 5, 0))
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_resize_augment_vs_oracle(dtype):
+    for sid in [1, 2, 3, 4]:
+        H, W = oracle.sample_hw(42, sid)
+        src = oracle.gen_sample(42, sid, H * W * 3)
+        got = device_augment(src[None], np.array([sid], np.uint64), H, W, 42, 2, mode="resize",
+                             dtype=dtype)[0]
+        want = oracle.augment(src.reshape(H, W, 3), sid, 42, 2, mode=oracle.AUG_RESIZE,
+                              bf16=dtype == "bf16")
+        if dtype == "fp32":
+            assert np.abs(got - want).max() <= FP32_TOL
+        else:
+            assert bf16_ulps(got, want) <= 1
+        assert np.array_equal(got, want)
+
+
+def test_augment_params_vs_oracle():
+    import ctypes as C
+    ids = np.arange(1000, dtype=np.uint64) * 7919
+    spec = AugmentConfig().to_c()
+    out = np.empty((1000, 5), np.uint32)
+    _capi.check(_capi.lib().ll_augment_params(ll.locload.context(), C.byref(spec), 42, 3,
+                                              _capi.ptr(ids, C.c_uint64), 1000, 256, 256,
+                                              _capi.ptr(out, C.c_uint32)))
+    for k in range(1000):
+        assert tuple(out[k]) == oracle.aug_params(42, 3, int(ids[k]), 256, 256)
+
+
+# ------------------------------------------------------------- loader
+def make_learners(d, p, B, exchange="p2p", scheme="locality_balanced", dtype="fp32", seed=42):
+    lds = []
+    for j in range(p):
+        cfg = LoaderConfig(d=d, learners=p, rank=j, batch_size=B, seed=seed, data_seed=seed,
+                           scheme=scheme, exchange=exchange,
+                           augment=AugmentConfig(out_dtype=dtype))
+        ld = DeviceLoader(cfg)
+        ld.populate()
+        lds.append(ld)
+    if p > 1 and exchange == "p2p":
+        DeviceLoader.link_peers(lds)
+    return lds
+
+
+def test_loader_cfg1_plan_vs_oracle(golden):
+    """cfg1 (d=10k, p=4, B=256): every step of epochs 0 and 1 vs the oracle,
+    and the epoch's moved / regular-remote totals vs the reference."""
+    ld = make_learners(10000, 4, 256)[0]
+    for epoch in [0, 1]:
+        ld.plan_epoch(epoch)
+        order = oracle.permute_epoch(42, epoch, 10000)
+        for t in range(ld.steps_per_epoch):
+            ids, off, kept, counts, mv = ld.plan_step(t)
+            r = oracle.assign_step(order[t * 256:(t + 1) * 256], 4, 10000,
+                                   oracle.MODE_LOCALITY_BALANCED)
+            assert np.array_equal(ids, r["final_ids"]) and np.array_equal(off, r["final_off"])
+            assert [m[:5] for m in mv] == [tuple(int(x) for x in m) for m in r["moves"]]
+        if epoch == 0:
+            tot = ld.epoch_totals()
+            ref = golden["remote_per_epoch"][0]
+            assert tot["moved"] == ref["loc_moved"] == 417
+            assert tot["reg_remote"] == ref["reg_remote"] == 7468
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_loader_cfg1_outputs_vs_oracle(dtype):
+    """Four learners on one GPU (P2P exchange over shared HBM): each learner's
+    augmented batch equals the oracle's augment of its final list."""
+    d, p, B = 10000, 4, 256
+    lds = make_learners(d, p, B, dtype=dtype)
+    order = oracle.permute_epoch(42, 1, d)
+    for t in [0, 7, 38]:
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, d, oracle.MODE_LOCALITY_BALANCED)
+        for j, ld in enumerate(lds):
+            info = ld.step(1, t)
+            lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            assert info.kept == r["kept"][j] and info.n_local == len(lst)
+            got = ld.fetch(info)
+            src = oracle.gen_samples(42, lst, 256 * 256 * 3)
+            for k, sid in enumerate(lst):
+                want = oracle.augment(src[k].reshape(256, 256, 3), int(sid), 42, 1,
+                                      bf16=dtype == "bf16")
+                assert np.array_equal(got[k], want), (t, j, k)
+
+
+def test_loader_regular_scheme_outputs():
+    d, p, B = 4096, 2, 128
+    lds = make_learners(d, p, B, scheme="regular")
+    order = oracle.permute_epoch(42, 0, d)
+    for t in [0, 5]:
+        batch = order[t * B:(t + 1) * B]
+        for j, ld in enumerate(lds):
+            info = ld.step(0, t)
+            lst = batch[j * B // p:(j + 1) * B // p]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            got = ld.fetch(info)
+            src = oracle.gen_samples(42, lst, 256 * 256 * 3)
+            for k, sid in enumerate(lst):
+                assert np.array_equal(got[k], oracle.augment(src[k].reshape(256, 256, 3),
+                                                             int(sid), 42, 0))
+
+
+def test_loader_host_step_equals_device_step():
+    """The reference-facing host call (GlobalBatch in, local ids out) delivers
+    exactly what the device-planned step delivers."""
+    d, p, B = 8192, 2, 512
+    lds = make_learners(d, p, B)
+    order = ll.permute_epoch(42, 2, d).order
+    for t in [0, 3]:
+        batch = np.ascontiguousarray(order[t * B:(t + 1) * B])
+        for ld in lds:
+            dev = ld.step(2, t)
+            a = ld.fetch(dev)
+            out_ids = np.empty(B, np.uint64)
+            host = ld.step_host(2, t, batch, out_ids)
+            assert host.n_local == dev.n_local and host.kept == dev.kept
+            assert np.array_equal(out_ids[:host.n_local], ld.fetch_ids(dev))
+            assert np.array_equal(ld.fetch(host), a)
+
+
+def test_loader_run_epoch_report():
+    """pipeline.hpp:55-64 accounting over a whole epoch (test_pipeline.cpp:125-133)."""
+    lds = make_learners(2000, 2, 64)
+    reps = [ld.run_epoch(0) for ld in lds]
+    assert all(r.batches == 31 for r in reps)
+    assert sum(r.samples for r in reps) == 31 * 64
+    assert all(r.cache_hits + r.cache_misses == r.samples for r in reps)
+    assert all(len(r.batch_latency_s) == 31 for r in reps)
+
+
+def test_loader_config_errors():
+    with pytest.raises(ValueError, match="CacheDirectory: cached fraction"):
+        DeviceLoader(LoaderConfig(alpha=1.5))
+    with pytest.raises(ValueError, match="batches: batch size"):
+        DeviceLoader(LoaderConfig(d=10, batch_size=11))
+    with pytest.raises(ValueError, match="reg_slice"):
+        DeviceLoader(LoaderConfig(d=100, learners=3, batch_size=10, scheme="regular"))
+    with pytest.raises(ValueError, match="Loader: workers, parallelism"):
+        DeviceLoader(LoaderConfig(prefetch_depth=0))
+    ld = DeviceLoader(LoaderConfig(d=1000, learners=2, batch_size=100))
+    with pytest.raises(ValueError, match="not populated"):
+        ld.step(0, 0)
+    ld.populate()
+    with pytest.raises(ValueError, match="exchange"):
+        for t in range(10):
+            ld.step(0, t)
