@@ -220,6 +220,7 @@ static void permute_to_host(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint64_t
                    n_forced);
     widen_device(ctx, order.as<uint32_t>(), wide.as<uint64_t>(), k_out);
     d2h_sync(ctx, host_order, wide.ptr, sizeof(uint64_t) * k_out);
+    permute_rounds(ctx);  // raises if the kernel's round guard tripped
 }
 
 // core.cpp:11-27

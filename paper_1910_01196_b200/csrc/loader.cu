@@ -133,7 +133,15 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     src.p = p;
     src.cached = ld->cached;
     src.sample_bytes = ld->S;
-    if (p > 1 && (n_send || n_recv)) {
+    if (p > 1 && c.scheme == LL_SCHEME_REGULAR) {
+        // reg_slice (sampling.cpp:27-42) ignores ownership: every sample of the
+        // slice is read from its owner's shard (the owner may be this learner).
+        require(c.exchange == LL_EXCHANGE_P2P && ld->peers_ready,
+                "loader: the regular scheme needs the P2P exchange (peer shards)");
+        src.kept = 0;
+        src.peers = ld->d_peers.as<const uint8_t*>();
+        n_recv = n_local;
+    } else if (p > 1 && (n_send || n_recv)) {
         if (c.exchange == LL_EXCHANGE_NCCL) {
             require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
             const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
@@ -169,7 +177,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
         info->epoch = epoch;
         info->step = step;
         info->n_local = n_local;
-        info->kept = kept;
+        info->kept = src.kept;
         info->received = n_recv;
         info->moved_total = h_stats[0];
         info->nvlink_bytes = nvl_recv * ld->S;
@@ -318,6 +326,7 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     assign_device(ld->ctx, ld->order.as<uint32_t>(), ld->steps, c.batch_size, c.learners,
                   ld->cached, c.scheme, ld->plan.view());
     copy_tables(ld, ld->plan, ld->steps);
+    permute_rounds(ld->ctx);  // raises if the kernel's round guard tripped
     ld->plan_epoch = static_cast<int64_t>(epoch);
 }
 

@@ -34,6 +34,7 @@ namespace {
 constexpr int kThreads = 512;
 constexpr uint32_t kSmallList = 16384;  // survivors handed to a single CTA
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kMaxRounds = 4096;   // O(log d) expected (~50 at d = 1.28 M); hang guard
 
 struct PermArgs {
     uint64_t s0;
@@ -171,7 +172,7 @@ __global__ void __launch_bounds__(kThreads) k_permute(PermArgs a) {
     uint32_t n = d;
     uint32_t round = 1;
     auto gsync = [&] { grid.sync(); };
-    while (n > kSmallList) {
+    while (n > kSmallList && round < kMaxRounds) {
         uint32_t* next = (cur == a.L0) ? a.L1 : a.L0;
         unsigned int* cnt = &a.ctl[4 + round % 3];
         if (gtid == 0) a.ctl[4 + (round + 1) % 3] = 0;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) k_permute(PermArgs a) {
     if (blockIdx.x != 0) return;
     // Tail rounds inside CTA 0 (all grid writes are visible after grid.sync).
     auto bsync = [] { __syncthreads(); };
-    while (n > 0) {
+    while (n > 0 && round < kMaxRounds) {
         uint32_t* next = (cur == a.L0) ? a.L1 : a.L0;
         unsigned int* cnt = &a.ctl[4 + round % 3];
         if (threadIdx.x == 0) a.ctl[4 + (round + 1) % 3] = 0;
@@ -190,7 +191,10 @@ __global__ void __launch_bounds__(kThreads) k_permute(PermArgs a) {
         cur = next;
         ++round;
     }
-    if (threadIdx.x == 0) a.ctl[2] = round - 1;
+    if (threadIdx.x == 0) {
+        a.ctl[2] = round - 1;
+        a.ctl[3] = n;  // survivors left: non-zero only if the round guard tripped
+    }
 }
 
 __global__ void k_widen(const uint32_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t n) {
@@ -242,11 +246,12 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
 }
 
 uint32_t permute_rounds(ll_ctx* ctx) {
-    unsigned int rounds = 0;
-    LL_CUDA(cudaMemcpyAsync(&rounds, ctx->buf("perm.ctl", 64).as<unsigned int>() + 2,
-                            sizeof(rounds), cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned int ctl[2] = {0, 0};
+    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf("perm.ctl", 64).as<unsigned int>() + 2, sizeof(ctl),
+                            cudaMemcpyDeviceToHost, ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
-    return rounds;
+    if (ctl[1] != 0) fail(LL_ERR_RUNTIME, "permute: round limit exceeded (internal error)");
+    return ctl[0];
 }
 
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n) {
