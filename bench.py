@@ -285,8 +285,9 @@ def run_ours(args):
     _capi.check(lib.ll_ctx_reset_stats(ctx))
     _capi.check(lib.ll_ctx_set_timing(ctx, 1))
     k2 = min(args.steps, 2 * spe)
+    start2 = start + ((args.steps + spe - 1) // spe) * spe  # fresh epochs: plans re-run
     barrier()
-    run_steps(start, k2)
+    run_steps(start2, k2)
     barrier()
     _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     stats = {}
