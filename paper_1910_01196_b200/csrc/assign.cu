@@ -21,6 +21,7 @@
 // definition; the reference only deals counts), so tail moves hand them over
 // first -- they cost no NVLink bytes.
 #include "ll_internal.h"
+#include "ll_rng.cuh"
 
 namespace ll {
 namespace {
@@ -58,7 +59,17 @@ struct AssignArgs {
     uint32_t p;
     uint64_t cached;
     int scheme;
+    AugPlan aug;
 };
+
+// Crop parameters of sample s (lo_aug_params_for, CROP mode), packed.
+__device__ __forceinline__ uint32_t crop_params(const AugPlan& g, uint32_t s) {
+    SplitMix r(derive_seed(g.seed, g.epoch, s));
+    const uint32_t y0 = static_cast<uint32_t>(r.bounded(static_cast<uint64_t>(g.H - g.ch) + 1));
+    const uint32_t x0 = static_cast<uint32_t>(r.bounded(static_cast<uint64_t>(g.W - g.cw) + 1));
+    const uint32_t flip = static_cast<uint32_t>(r.next() >> 63);
+    return y0 | (x0 << 15) | (flip << 31);
+}
 
 __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
     const uint32_t st = blockIdx.x;
@@ -163,6 +174,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
         const uint32_t s = batch[e];
         if (a.scheme == LL_SCHEME_REGULAR) {
             final_ids[e] = s;
+            if (a.aug.enabled) P.aug[st * B + e] = crop_params(a.aug, s);
             continue;
         }
         const uint32_t v = scratch[e];
@@ -188,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
             }
         }
         final_ids[off[fj] + fk] = s;
+        if (a.aug.enabled) P.aug[st * B + off[fj] + fk] = crop_params(a.aug, s);
     }
     (void)my_nvl_moved;
     __syncthreads();
@@ -242,12 +255,14 @@ PlanDev PlanBufs::view() const {
     v.n_moves = n_moves.as<uint32_t>();
     v.stats = stats.as<uint32_t>();
     v.scratch = scratch.as<uint32_t>();
+    v.aug = aug.as<uint32_t>();
     return v;
 }
 
 void PlanBufs::reserve(uint64_t steps, uint64_t B) {
     final_ids.reserve(sizeof(uint32_t) * steps * B);
     scratch.reserve(sizeof(uint32_t) * steps * B);
+    aug.reserve(sizeof(uint32_t) * steps * B);
     off.reserve(sizeof(uint32_t) * steps * (kMaxP + 1));
     kept.reserve(sizeof(uint32_t) * steps * kMaxP);
     counts.reserve(sizeof(uint32_t) * steps * kMaxP);
@@ -257,13 +272,16 @@ void PlanBufs::reserve(uint64_t steps, uint64_t B) {
 }
 
 void assign_device(ll_ctx* ctx, const uint32_t* d_order, uint64_t steps, uint64_t B, uint32_t p,
-                   uint64_t cached, int scheme, const PlanDev& plan) {
+                   uint64_t cached, int scheme, const PlanDev& plan, const AugPlan& aug) {
     require(p >= 1 && p <= kMaxP, "assign: learner count must be in [1, 64]");
     require(B < (1ull << 24), "assign: batch size must be < 2^24");
     if (scheme == LL_SCHEME_REGULAR)
         require(B % p == 0, "reg_slice: learner count must divide the batch size");
     if (steps == 0) return;
-    AssignArgs a{d_order, B, p, cached, scheme};
+    require(!aug.enabled || (plan.aug != nullptr && aug.H >= aug.ch && aug.W >= aug.cw &&
+                             aug.H < 32768 && aug.W < 32768),
+            "assign: bad crop-parameter plan");
+    AssignArgs a{d_order, B, p, cached, scheme, aug};
     launch(ctx, "assign", [&] {
         k_assign<<<static_cast<unsigned>(steps), kThreads, 0, ctx->stream>>>(a, plan);
     });

@@ -21,6 +21,8 @@
 
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 namespace ll {
 namespace {
 
@@ -108,12 +110,133 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
            (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
 }
 
+// Packed fp32x2 helpers (FADD2 / FMUL2 on sm_100): two IEEE-rounded ops per
+// instruction, bit-identical to the scalar sequence.
+__device__ __forceinline__ uint64_t pk(uint32_t lo, uint32_t hi) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+    return r;
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint32_t lo32(uint64_t v) { return static_cast<uint32_t>(v); }
+__device__ __forceinline__ uint32_t hi32(uint64_t v) { return static_cast<uint32_t>(v >> 32); }
+
+// float(byte j of w) - 2^23 == byte exactly: PRMT builds 0x4B0000bb (2^23 + bb).
+template <int J>
+__device__ __forceinline__ uint32_t magic_byte(uint32_t w) {
+    return __byte_perm(w, 0x4B000000u, 0x7440u | static_cast<uint32_t>(J));
+}
+
+// Two output pixels (same channel): ((float(v) - mean255) * inv_std255) each.
+__device__ __forceinline__ uint64_t norm2(uint32_t m0, uint32_t m1, uint64_t mean2,
+                                          uint64_t inv2) {
+    const uint64_t big = 0x4B0000004B000000ull;  // {2^23, 2^23}
+    return mul2(sub2(sub2(pk(m0, m1), big), mean2), inv2);
+}
+
+__device__ __forceinline__ uint32_t bf16x2(uint64_t v) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(__uint_as_float(lo32(v)), __uint_as_float(hi32(v)));
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// One thread's share of one output row: PX consecutive output pixels of all
+// three planes.  `row` holds the crop row's source bytes from a0 (16-byte
+// aligned) on; `base` is the byte offset of the lowest source pixel of the
+// run.  The 3*PX source bytes are fetched as 32-bit words (4 or 7 LDS) and
+// realigned with funnel shifts (the shift is uniform per sample); each byte
+// becomes a float through PRMT + exact subtraction, and the normalisation
+// runs on packed fp32x2 -- no I2F, same IEEE results as the oracle.
+template <bool BF16, bool FLIP, int DBG = 0>
+__device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint64_t const* mean2,
+                                         uint64_t const* inv2, void* out, uint64_t o,
+                                         uint64_t plane) {
+    constexpr int PX = BF16 ? 8 : 4;
+    constexpr int NB = 3 * PX;      // 12 or 24 source bytes
+    constexpr int NW = NB / 4 + 1;  // words covering them at any alignment
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (base >> 2);
+    const uint32_t sh = 8u * static_cast<uint32_t>(base & 3);
+    uint32_t raw[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) raw[i] = w[i];
+    uint32_t by[NB / 4];
+#pragma unroll
+    for (int i = 0; i < NB / 4; ++i) by[i] = __funnelshift_r(raw[i], raw[i + 1], sh);
+    auto mb = [&](int j) -> uint32_t {
+        const uint32_t x = by[j >> 2];
+        switch (j & 3) {
+            case 0: return magic_byte<0>(x);
+            case 1: return magic_byte<1>(x);
+            case 2: return magic_byte<2>(x);
+            default: return magic_byte<3>(x);
+        }
+    };
+    uint64_t v[3][PX / 2];
+#pragma unroll
+    for (int u = 0; u < PX; u += 2) {
+        const int p0 = FLIP ? (PX - 1 - u) : u;
+        const int p1 = FLIP ? (PX - 2 - u) : u + 1;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[c][u / 2] = norm2(mb(3 * p0 + c), mb(3 * p1 + c), mean2[c], inv2[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        if (DBG == 2 && lo32(v[c][0]) != 0x12345u) continue;  // debug: compute, no stores
+        if constexpr (BF16) {
+            st_cs_v4(static_cast<uint16_t*>(out) + o + c * plane,
+                     make_uint4(bf16x2(v[c][0]), bf16x2(v[c][1]), bf16x2(v[c][2]),
+                                bf16x2(v[c][3])));
+        } else {
+            st_cs_v4(static_cast<float*>(out) + o + c * plane,
+                     make_uint4(lo32(v[c][0]), hi32(v[c][0]), lo32(v[c][1]), hi32(v[c][1])));
+        }
+    }
+}
+
+// Rows [r_first, r_first + kBand) of the band: thread (tr, tq) writes pixel run
+// tq of rows tr, tr + PX, ...
+template <bool BF16, int DBG = 0>
+__device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, uint32_t a0,
+                                          uint64_t k, uint32_t band, const NormConst& nc,
+                                          void* out) {
+    constexpr uint32_t PX = BF16 ? 8 : 4;
+    constexpr uint32_t TPR = kOut / PX;
+    const uint32_t tr = threadIdx.x / TPR, tq = threadIdx.x - tr * TPR;
+    const uint64_t plane = static_cast<uint64_t>(kOut) * kOut;
+    const uint64_t obase = k * 3 * plane + static_cast<uint64_t>(band * kBand) * kOut + tq * PX;
+    const int32_t base = q.flip ? static_cast<int32_t>(3 * (q.x0 + kOut - PX - tq * PX)) -
+                                      static_cast<int32_t>(a0)
+                                : static_cast<int32_t>(3 * (q.x0 + tq * PX)) -
+                                      static_cast<int32_t>(a0);
+    uint64_t mean2[3], inv2[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        mean2[c] = pk(__float_as_uint(nc.mean255[c]), __float_as_uint(nc.mean255[c]));
+        inv2[c] = pk(__float_as_uint(nc.inv_std255[c]), __float_as_uint(nc.inv_std255[c]));
+    }
+#pragma unroll 1
+    for (uint32_t rr = 0; rr < kBand / PX; ++rr) {
+        const uint32_t r = rr * PX + tr;
+        const uint64_t o = obase + static_cast<uint64_t>(r) * kOut;
+        if (q.flip)
+            emit_run<BF16, true, DBG>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
+        else
+            emit_run<BF16, false, DBG>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
+    }
+}
+
 // PX output pixels per thread: 4 (fp32, one float4 per plane) or 8 (bf16,
 // eight bf16 per plane).  kThreads/(224/PX) = PX rows per pass.
-template <bool BF16>
+template <bool BF16, int DBG = 0>
 __global__ void __launch_bounds__(kThreads) k_augment_crop(AugArgs a) {
-    constexpr uint32_t PX = BF16 ? 8 : 4;
-    constexpr uint32_t TPR = kOut / PX;  // threads per output row
     __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
     __shared__ const uint8_t* s_src;
     __shared__ Params s_prm;
@@ -126,7 +249,13 @@ __global__ void __launch_bounds__(kThreads) k_augment_crop(AugArgs a) {
         const uint8_t* src;
         resolve(a.src, k, &id, &src);
         s_src = src;
-        s_prm = aug_params(a.seed, a.epoch, id, a.H, a.W, kOut, kOut, LL_AUG_CROP);
+        if (a.src.aug) {  // precomputed by the plan (assign.cu crop_params)
+            const uint32_t* ap = a.src.list_off ? a.src.aug + *a.src.list_off : a.src.aug;
+            const uint32_t w = ap[k];
+            s_prm = Params{w & 0x7FFFu, (w >> 15) & 0xFFFFu, kOut, kOut, w >> 31};
+        } else {
+            s_prm = aug_params(a.seed, a.epoch, id, a.H, a.W, kOut, kOut, LL_AUG_CROP);
+        }
     }
     __syncthreads();
     const Params q = s_prm;
@@ -135,53 +264,26 @@ __global__ void __launch_bounds__(kThreads) k_augment_crop(AugArgs a) {
     const uint32_t a0 = (3 * q.x0) & ~15u;
     const uint32_t nch = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
     const uint8_t* gbase = src + static_cast<uint64_t>(q.y0 + band * kBand) * row_bytes + a0;
-    for (uint32_t t = tid; t < kBand * nch; t += kThreads) {
-        const uint32_t r = t / nch, c = t - r * nch;
-        const uint4 v = ld_nc_v4(gbase + static_cast<uint64_t>(r) * row_bytes + 16 * c);
-        *reinterpret_cast<uint4*>(&rows[r][16 * c]) = v;
+    if (DBG != 1) {  // debug 1: no source loads
+        // every load of the band in flight at once: slot t -> (row t/44, chunk t%44)
+        constexpr uint32_t kSlots = kRowSmem / 16;  // 44 >= 43 chunks per row
+        constexpr uint32_t kIters = (kBand * kSlots + kThreads - 1) / kThreads;
+        uint4 v[kIters];
+#pragma unroll
+        for (uint32_t i = 0; i < kIters; ++i) {
+            const uint32_t t = tid + i * kThreads, r = t / kSlots, c = t - r * kSlots;
+            if (r < kBand && c < nch)
+                v[i] = ld_nc_v4(gbase + static_cast<uint64_t>(r) * row_bytes + 16 * c);
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < kIters; ++i) {
+            const uint32_t t = tid + i * kThreads, r = t / kSlots, c = t - r * kSlots;
+            if (r < kBand && c < nch) *reinterpret_cast<uint4*>(&rows[r][16 * c]) = v[i];
+        }
     }
     __syncthreads();
 
-    const uint32_t tr = tid / TPR, tq = tid - tr * TPR;
-    const uint64_t plane = static_cast<uint64_t>(kOut) * kOut;
-    const uint64_t obase = k * 3 * plane;
-    // byte offset (within the smem row) of output pixel tq*PX + u
-    int32_t b0, step;
-    if (q.flip) {
-        b0 = static_cast<int32_t>(3 * (q.x0 + kOut - 1 - tq * PX)) - static_cast<int32_t>(a0);
-        step = -3;
-    } else {
-        b0 = static_cast<int32_t>(3 * (q.x0 + tq * PX)) - static_cast<int32_t>(a0);
-        step = 3;
-    }
-#pragma unroll 1
-    for (uint32_t it = 0; it < kBand / PX; ++it) {
-        const uint32_t r = it * PX + tr;
-        const uint32_t oy = band * kBand + r;
-        const uint8_t* row = rows[r];
-        float v[3][PX];
-#pragma unroll
-        for (uint32_t u = 0; u < PX; ++u) {
-            const int32_t b = b0 + step * static_cast<int32_t>(u);
-#pragma unroll
-            for (uint32_t c = 0; c < 3; ++c) v[c][u] = norm(row[b + c], a.nc.mean255[c], a.nc.inv_std255[c]);
-        }
-        const uint64_t o = obase + static_cast<uint64_t>(oy) * kOut + tq * PX;
-#pragma unroll
-        for (uint32_t c = 0; c < 3; ++c) {
-            if constexpr (BF16) {
-                uint16_t* out = static_cast<uint16_t*>(a.out);
-                st_cs_v4(out + o + c * plane,
-                         make_uint4(pack_bf16(v[c][0], v[c][1]), pack_bf16(v[c][2], v[c][3]),
-                                    pack_bf16(v[c][4], v[c][5]), pack_bf16(v[c][6], v[c][7])));
-            } else {
-                float* out = static_cast<float*>(a.out);
-                st_cs_v4(out + o + c * plane,
-                         make_uint4(__float_as_uint(v[c][0]), __float_as_uint(v[c][1]),
-                                    __float_as_uint(v[c][2]), __float_as_uint(v[c][3])));
-            }
-        }
-    }
+    emit_band<BF16, DBG>(&rows[0][0], q, a0, k, band, a.nc, a.out);
 }
 
 // K7: variable geometry, bilinear resize (half-pixel centres, edge clamp).
@@ -262,6 +364,17 @@ NormConst norm_constants(const ll_augment_spec& s) {
     return c;
 }
 
+// Debug knob for measurements only (LL_AUG_DEBUG): 1 = skip source loads,
+// 2 = skip output stores.  Results are wrong by construction; never set in
+// product runs.
+static int crop_debug() {
+    static int v = [] {
+        const char* e = getenv("LL_AUG_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 static void validate_spec(const ll_augment_spec& spec, uint32_t H, uint32_t W) {
     require(spec.out_dtype == LL_OUT_F32 || spec.out_dtype == LL_OUT_BF16,
             "augment: out_dtype must be fp32 or bf16");
@@ -294,8 +407,15 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
     const bool bf16 = spec.out_dtype == LL_OUT_BF16;
     if (spec.mode == LL_AUG_CROP) {
         const dim3 grid(static_cast<unsigned>(n * kBands));
+        const int dbg = crop_debug();
         launch(ctx, "augment_crop", [&] {
-            if (bf16)
+            if (dbg == 1)
+                bf16 ? k_augment_crop<true, 1><<<grid, kThreads, 0, ctx->stream>>>(a)
+                     : k_augment_crop<false, 1><<<grid, kThreads, 0, ctx->stream>>>(a);
+            else if (dbg == 2)
+                bf16 ? k_augment_crop<true, 2><<<grid, kThreads, 0, ctx->stream>>>(a)
+                     : k_augment_crop<false, 2><<<grid, kThreads, 0, ctx->stream>>>(a);
+            else if (bf16)
                 k_augment_crop<true><<<grid, kThreads, 0, ctx->stream>>>(a);
             else
                 k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);

@@ -119,14 +119,23 @@ struct PlanDev {
     uint32_t* n_moves = nullptr;    // [steps]
     uint32_t* stats = nullptr;      // [steps][4]: moved, nvlink, uncached, reg_remote
     uint32_t* scratch = nullptr;    // [steps][B]
+    uint32_t* aug = nullptr;        // [steps][B] packed crop params per final slot (or null)
+};
+// Crop parameters the plan precomputes for every final slot (crop mode):
+// packed y0 | x0 << 15 | flip << 31 (lo_aug_params_for).
+struct AugPlan {
+    bool enabled = false;
+    uint64_t seed = 0, epoch = 0;
+    uint32_t H = 0, W = 0, ch = 0, cw = 0;
 };
 struct PlanBufs {
-    DevBuf final_ids, off, kept, counts, moves, n_moves, stats, scratch;
+    DevBuf final_ids, off, kept, counts, moves, n_moves, stats, scratch, aug;
     PlanDev view() const;
     void reserve(uint64_t steps, uint64_t B);
 };
 void assign_device(ll_ctx* ctx, const uint32_t* d_order, uint64_t steps, uint64_t B, uint32_t p,
-                   uint64_t cached, int scheme, const PlanDev& plan);
+                   uint64_t cached, int scheme, const PlanDev& plan,
+                   const AugPlan& aug = AugPlan());
 void balance_device(ll_ctx* ctx, const int64_t* d_counts, const int64_t* d_targets, uint32_t p,
                     uint64_t n, ll_move* d_moves, uint32_t* d_n);
 
@@ -154,6 +163,7 @@ struct SrcMap {
     const uint32_t* list_off = nullptr;  // if set: list += *list_off (device)
     uint32_t kept = 0;
     const uint32_t* kept_dev = nullptr;  // if set: kept = *kept_dev (device)
+    const uint32_t* aug = nullptr;       // plan-precomputed crop params, list-aligned
     const uint8_t* shard = nullptr;
     uint64_t shard_first = 0;
     const uint8_t* recv = nullptr;     // NCCL path: received samples in list order

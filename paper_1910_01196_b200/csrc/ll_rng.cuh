@@ -47,12 +47,20 @@ LL_HD uint64_t umulhi64(uint64_t a, uint64_t b) {
 // One Lemire trial: returns true when draw r is accepted for range n and
 // writes the result.  threshold = (2^64 - n) mod n < n, so lo >= n accepts
 // without the 64-bit modulo (taken with probability < n / 2^64).
+// The 64-bit modulo is kept out of line so the compiler cannot hoist it onto
+// the (almost always taken) fast path.
+#if defined(__CUDACC__)
+static __host__ __device__ __noinline__
+#else
+inline
+#endif
+uint64_t lemire_threshold(uint64_t n) { return (0 - n) % n; }
+
 LL_HD bool lemire_accept(uint64_t r, uint64_t n, uint64_t* out) {
     const uint64_t lo = r * n;
     *out = umulhi64(r, n);
     if (lo >= n) return true;
-    const uint64_t threshold = (0 - n) % n;
-    return lo >= threshold;
+    return lo >= lemire_threshold(n);
 }
 
 struct SplitMix {

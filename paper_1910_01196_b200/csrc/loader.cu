@@ -93,6 +93,20 @@ void copy_tables(ll_loader* ld, const PlanBufs& plan, uint64_t steps) {
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+AugPlan aug_plan(const ll_loader* ld, uint64_t epoch) {
+    AugPlan g;
+    const ll_loader_config& c = ld->cfg;
+    if (c.augment.mode != LL_AUG_CROP) return g;
+    g.enabled = true;
+    g.seed = c.seed;
+    g.epoch = epoch;
+    g.H = c.height;
+    g.W = c.width;
+    g.ch = c.augment.out_h;
+    g.cw = c.augment.out_w;
+    return g;
+}
+
 void ensure_out(ll_loader* ld) {
     if (!ld->out.empty()) return;
     const ll_loader_config& c = ld->cfg;
@@ -133,6 +147,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     src.p = p;
     src.cached = ld->cached;
     src.sample_bytes = ld->S;
+    if (c.augment.mode == LL_AUG_CROP) src.aug = pd.aug + step * B + h_off[me];
     if (p > 1 && c.scheme == LL_SCHEME_REGULAR) {
         // reg_slice (sampling.cpp:27-42) ignores ownership: every sample of the
         // slice is read from its owner's shard (the owner may be this learner).
@@ -324,7 +339,7 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     permute_device(ld->ctx, c.seed, epoch, static_cast<uint32_t>(c.d), ld->order.as<uint32_t>(),
                    nullptr, 0);
     assign_device(ld->ctx, ld->order.as<uint32_t>(), ld->steps, c.batch_size, c.learners,
-                  ld->cached, c.scheme, ld->plan.view());
+                  ld->cached, c.scheme, ld->plan.view(), aug_plan(ld, epoch));
     copy_tables(ld, ld->plan, ld->steps);
     permute_rounds(ld->ctx);  // raises if the kernel's round guard tripped
     ld->plan_epoch = static_cast<int64_t>(epoch);
@@ -354,7 +369,7 @@ void loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64
                             cudaMemcpyHostToDevice, ctx->stream));
     narrow_device(ctx, ld->e2e_batch64.as<uint64_t>(), ld->e2e_order.as<uint32_t>(), B);
     assign_device(ctx, ld->e2e_order.as<uint32_t>(), 1, B, c.learners, ld->cached, c.scheme,
-                  ld->e2e_plan.view());
+                  ld->e2e_plan.view(), aug_plan(ld, epoch));
     // the host needs this step's counts to size the grid and the messages
     ll_move h_moves[kMaxP];
     uint32_t h_off[kMaxP + 1], h_kept[kMaxP], h_n = 0, h_stats[4];
