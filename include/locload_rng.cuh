@@ -1,4 +1,5 @@
-// ll_rng.cuh -- counter-based splitmix64, shared by host and device code.
+// locload_rng.cuh -- counter-based splitmix64, shared by host and device code
+// (the CUDA kernels and the C++ API in include/locload/rng.hpp).
 //
 // Bit-identical to proj/include/locload/rng.hpp: mix64 (:9-13), derive_seed
 // (:19-26), SplitMix64::next (:35-38) and the Lemire bounded draw (:41-50).

@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "liblocload_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 SOURCES = ["capi.cu", "permute.cu", "assign.cu", "shard.cu", "augment.cu", "exchange.cu",
-           "loader.cu"]
+           "loader.cu", "host/locload_api.cpp"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2,-Wall", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]
@@ -27,8 +27,11 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(ROOT, "include", "locload_b200.h"))
+    deps = [os.path.join(d, f) for d in (CSRC, os.path.join(CSRC, "host"))
+            for f in os.listdir(d) if os.path.isfile(os.path.join(d, f))]
+    inc = os.path.join(ROOT, "include")
+    for d, _, fs in os.walk(inc):
+        deps += [os.path.join(d, f) for f in fs]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -40,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     logs = []
     for src in SOURCES:
-        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        obj = os.path.join(objdir, os.path.basename(src).rsplit(".", 1)[0] + ".o")
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)

@@ -21,7 +21,7 @@
 // definition; the reference only deals counts), so tail moves hand them over
 // first -- they cost no NVLink bytes.
 #include "ll_internal.h"
-#include "ll_rng.cuh"
+#include "locload_rng.cuh"
 
 namespace ll {
 namespace {

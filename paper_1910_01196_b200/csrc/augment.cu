@@ -17,7 +17,7 @@
 // PX consecutive output pixels of all three planes as 128-bit streaming
 // stores, so every warp writes 512 contiguous bytes per plane row.
 #include "ll_internal.h"
-#include "ll_rng.cuh"
+#include "locload_rng.cuh"
 
 #include <cuda_bf16.h>
 

@@ -24,7 +24,7 @@
 #include <cooperative_groups.h>
 
 #include "ll_internal.h"
-#include "ll_rng.cuh"
+#include "locload_rng.cuh"
 
 namespace cg = cooperative_groups;
 

@@ -6,7 +6,7 @@
 // every 16-byte chunk (draws 2c, 2c+1) is independent: one thread writes one
 // 128-bit chunk with a streaming store.  Write-bound: HBM roofline.
 #include "ll_internal.h"
-#include "ll_rng.cuh"
+#include "locload_rng.cuh"
 
 namespace ll {
 namespace {
