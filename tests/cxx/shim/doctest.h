@@ -12,7 +12,12 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <algorithm>
 #include <functional>
+#include <map>
+#include <numeric>
+#include <set>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>

@@ -5,8 +5,6 @@
 #define DOCTEST_CONFIG_IMPLEMENT_WITH_MAIN
 #include <doctest.h>
 
-#include <cuda_runtime.h>
-
 #include <vector>
 
 #include "locload/balance.hpp"
@@ -52,6 +50,8 @@ TEST_CASE("device loader delivers the balanced locality lists in step order") {
     const auto plan = batches(permute_epoch(42, 3, 4096), 256);
     const CacheDirectory dir(4096, 2, 1.0);
     std::uint64_t expected_step = 0;
+    ll_ctx* host_copy = nullptr;
+    REQUIRE(ll_ctx_create(&host_copy, 0) == LL_OK);
     const gpu::EpochReport rep = a.run_epoch(3, [&](const gpu::DeviceBatch& batch) {
         CHECK(batch.step == expected_step);
         // learner 0's list: its cached samples then balance-moved ones
@@ -67,12 +67,15 @@ TEST_CASE("device loader delivers the balanced locality lists in step order") {
             if (m.sender == 0) mine.resize(mine.size() - m.count);
         }
         std::vector<std::uint32_t> got(batch.size);
-        cudaMemcpy(got.data(), batch.ids, 4 * batch.size, cudaMemcpyDeviceToHost);
+        REQUIRE(ll_ctx_copy_to_host(host_copy, got.data(),
+                                    reinterpret_cast<std::uintptr_t>(batch.ids),
+                                    4 * batch.size) == LL_OK);
         REQUIRE(got.size() == mine.size());
         for (std::size_t i = 0; i < got.size(); ++i) CHECK(got[i] == mine[i]);
         CHECK(batch.local + batch.received == batch.size);
         ++expected_step;
     });
+    ll_ctx_destroy(host_copy);
     CHECK(rep.batches == 16);
     CHECK(rep.samples == 16 * 128);
     CHECK(rep.cache_hits + rep.cache_misses == rep.samples);
