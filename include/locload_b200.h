@@ -78,6 +78,9 @@ int ll_permute_epoch_forced(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint64_t
                             uint64_t* host_order);
 /* rounds of the last permutation (deterministic-reservation commit rounds) */
 int ll_last_permute_rounds(ll_ctx* ctx, uint32_t* out);
+/* phase profile of the last permutation (globaltimer): {rounds, grid-wide
+ * rounds, ns draws+repair, ns grid-wide rounds, ns single-CTA rounds, ns total} */
+int ll_last_permute_profile(ll_ctx* ctx, uint64_t* out6);
 
 /* ---- sampling + balance: sampling.hpp:42-67, balance.hpp:20-50,
  *      equivalence.cpp:66-91 ------------------------------------------------ */

@@ -83,6 +83,7 @@ PROTOTYPES = {
     "ll_permute_epoch_forced": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, u64p,
                                           C.c_uint64, u64p]),
     "ll_last_permute_rounds": (C.c_int, [C.c_void_p, u32p]),
+    "ll_last_permute_profile": (C.c_int, [C.c_void_p, u64p]),
     "ll_assign": (C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double,
                             C.c_int, u64p, u64p, u64p, u64p, C.POINTER(Move), u32p, u64p]),
     "ll_balance_batch": (C.c_int, [C.c_void_p, i64p, i64p, C.c_uint32, C.c_uint64,

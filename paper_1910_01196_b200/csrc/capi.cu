@@ -14,6 +14,7 @@
 namespace ll {
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
 uint32_t permute_rounds(ll_ctx* ctx);
+void permute_profile(ll_ctx* ctx, uint64_t* out6);
 void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg);
 void loader_destroy(ll_loader* ld);
 void loader_comm_init(ll_loader* ld, const uint8_t* id128);
@@ -252,6 +253,13 @@ int ll_permutation_prefix(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint64_t d
         require(k <= d, "permutation_prefix: prefix length exceeds dataset size");
         if (k == 0) return;
         permute_to_host(ctx, seed, epoch, d, nullptr, 0, host_prefix, k);
+    });
+}
+
+int ll_last_permute_profile(ll_ctx* ctx, uint64_t* out6) {
+    return guarded([&] {
+        check_ctx(ctx);
+        permute_profile(ctx, out6);
     });
 }
 

@@ -19,8 +19,8 @@
 //     J[i] == i are no-ops and are dropped.
 //
 // Priorities are (round << 32 | ~i) under atomicMax, so R needs no reset
-// between rounds.  One cooperative persistent kernel runs everything; once the
-// survivor list is small, CTA 0 finishes alone with block barriers.
+// between rounds.  One cooperative persistent kernel runs everything; once at
+// most 2,048 iterations survive, CTA 0 finishes them in shared memory.
 #include <cooperative_groups.h>
 
 #include "ll_internal.h"
@@ -32,7 +32,6 @@ namespace ll {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr uint32_t kSmallList = 16384;  // survivors handed to a single CTA
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 constexpr uint32_t kMaxRounds = 4096;   // O(log d) expected (~50 at d = 1.28 M); hang guard
 
@@ -42,8 +41,8 @@ struct PermArgs {
     uint32_t* A;               // order being permuted
     uint32_t* J;               // swap partner of iteration i
     unsigned long long* R;     // reservations
-    uint32_t* L0;              // survivor lists
-    uint32_t* L1;
+    uint2* L0;                 // survivor lists of (i, J[i])
+    uint2* L1;
     unsigned int* ctl;         // [0..1] reject cells, [2] rounds, [4..6] list counters
     unsigned long long* shift; // extra draws consumed before the current index
     const uint64_t* forced;    // sorted forced-reject draw indices (test hook)
@@ -51,6 +50,11 @@ struct PermArgs {
 };
 
 __device__ __forceinline__ uint32_t ldcg(const uint32_t* p) { return __ldcg(p); }
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ unsigned long long ldcg64(const unsigned long long* p) {
     return __ldcg(p);
 }
@@ -79,51 +83,191 @@ __device__ __forceinline__ unsigned long long prio(uint32_t round, uint32_t i) {
 }
 
 // One reserve+commit round over `n` pending iterations read from `cur`
-// (or the identity when cur == nullptr) by threads [t0, t0+nth).
-template <typename Sync>
-__device__ __forceinline__ uint32_t run_round(const PermArgs& a, const uint32_t* cur, uint32_t n,
-                                              uint32_t* next, unsigned int* next_cnt,
-                                              uint32_t round, uint32_t gtid, uint32_t nth,
-                                              Sync&& sync) {
-    for (uint32_t t = gtid; t < n; t += nth) {
-        const uint32_t i = cur ? ldcg(cur + t) : t;
-        const uint32_t j = ldcg(a.J + i);
-        if (j == i) continue;
-        const unsigned long long key = prio(round, i);
-        atomicMax(a.R + i, key);
-        atomicMax(a.R + j, key);
+// (or the identity when cur == nullptr) by threads [gtid, +nth).  Each thread
+// works on kU iterations at a time with every load of the batch issued before
+// any is consumed (memory-level parallelism: the loads are dependent chains
+// cur -> J -> R -> A through L2).
+constexpr uint32_t kU = 4;
+
+// Survivor lists hold (i, J[i]) pairs so a round needs no J lookup; the first
+// round walks the identity and reads J.
+__device__ __forceinline__ void load_pairs(const PermArgs& a, const uint2* cur, uint32_t n,
+                                           uint32_t t0, uint32_t nth, uint32_t* i, uint32_t* j) {
+#pragma unroll
+    for (uint32_t u = 0; u < kU; ++u) {
+        const uint32_t t = t0 + u * nth;
+        if (t >= n) {
+            i[u] = j[u] = 0xFFFFFFFFu;
+        } else if (cur) {
+            const uint2 v = __ldcg(cur + t);
+            i[u] = v.x;
+            j[u] = v.y;
+        } else {
+            i[u] = t;
+            j[u] = ldcg(a.J + t);
+        }
     }
-    sync();
+}
+
+__device__ __forceinline__ uint32_t run_round(const PermArgs& a, const uint2* cur, uint32_t n,
+                                              uint2* next, unsigned int* next_cnt,
+                                              uint32_t round, uint32_t gtid, uint32_t nth,
+                                              cg::grid_group& grid) {
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t nth_w = nth & ~31u;  // nth is a multiple of 32
-    for (uint32_t tb = gtid - lane; tb < n; tb += nth_w) {
-        const uint32_t t = tb + lane;
-        bool pend = false;
-        uint32_t i = 0;
-        if (t < n) {
-            i = cur ? ldcg(cur + t) : t;
-            const uint32_t j = ldcg(a.J + i);
-            if (j != i) {
-                const unsigned long long key = prio(round, i);
-                if (ldcg64(a.R + i) == key && ldcg64(a.R + j) == key) {
-                    const uint32_t vi = ldcg(a.A + i), vj = ldcg(a.A + j);
-                    a.A[i] = vj;
-                    a.A[j] = vi;
+    const uint32_t wbase = gtid - lane;  // nth is a multiple of 32
+    for (uint32_t tb = wbase; tb < n; tb += nth * kU) {
+        uint32_t i[kU], j[kU];
+        load_pairs(a, cur, n, tb + lane, nth, i, j);
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) {
+            if (j[u] == i[u]) continue;  // padding or a no-op swap
+            const unsigned long long key = prio(round, i[u]);
+            atomicMax(a.R + i[u], key);
+            atomicMax(a.R + j[u], key);
+        }
+    }
+    grid.sync();
+    for (uint32_t tb = wbase; tb < n; tb += nth * kU) {
+        uint32_t i[kU], j[kU];
+        unsigned long long ri[kU], rj[kU];
+        load_pairs(a, cur, n, tb + lane, nth, i, j);
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) {
+            ri[u] = rj[u] = 0;
+            if (j[u] != i[u]) {
+                ri[u] = ldcg64(a.R + i[u]);
+                rj[u] = ldcg64(a.R + j[u]);
+            }
+        }
+        bool win[kU];
+        uint32_t vi[kU], vj[kU];
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) {
+            const unsigned long long key = prio(round, i[u]);
+            win[u] = j[u] != i[u] && ri[u] == key && rj[u] == key;
+            if (win[u]) {
+                vi[u] = ldcg(a.A + i[u]);
+                vj[u] = ldcg(a.A + j[u]);
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kU; ++u) {
+            if (win[u]) {
+                a.A[i[u]] = vj[u];
+                a.A[j[u]] = vi[u];
+            }
+            const bool pend = j[u] != i[u] && !win[u];
+            const unsigned mask = __ballot_sync(0xffffffffu, pend);
+            if (mask) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(next_cnt, __popc(mask));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (pend) next[base + __popc(mask & ((1u << lane) - 1u))] = make_uint2(i[u], j[u]);
+            }
+        }
+    }
+    grid.sync();
+    return ldcg(next_cnt);
+}
+
+// The last <= kTail survivors, inside CTA 0 and its shared memory: the <= 2*kTail
+// positions they touch are gathered into an open-addressing table (position ->
+// slot holding its current order value), the remaining rounds reserve with
+// shared-memory atomicMin on the iteration index and swap slot values, and the
+// slots are written back at the end.  Same deterministic-reservation rule,
+// so the result is unchanged; only the memory the rounds run in differs.
+constexpr uint32_t kTail = 2048;
+constexpr uint32_t kTab = 8192;            // power of two >= 2 * kTail / 0.5
+constexpr uint32_t kEmpty = 0xFFFFFFFFu;
+constexpr size_t kTailSmem = (3ull * kTab + 5ull * kTail + 4) * sizeof(uint32_t);
+
+__device__ __forceinline__ uint32_t tab_slot(uint32_t* keys, uint32_t* aval, const uint32_t* A,
+                                             uint32_t pos) {
+    uint32_t h = (pos * 2654435761u) >> (32 - 13);  // log2(kTab) = 13
+    for (;;) {
+        const uint32_t prev = atomicCAS(&keys[h], kEmpty, pos);
+        if (prev == kEmpty) {
+            aval[h] = ldcg(A + pos);
+            return h;
+        }
+        if (prev == pos) return h;
+        h = (h + 1) & (kTab - 1);
+    }
+}
+
+__device__ uint32_t smem_tail(const PermArgs& a, const uint2* cur, uint32_t n, uint32_t round) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* keys = sm;
+    uint32_t* aval = keys + kTab;
+    uint32_t* rsv = aval + kTab;
+    uint32_t* sidx = rsv + kTab;               // iteration index i of local survivor t
+    uint32_t* si = sidx + kTail;               // slot of position i
+    uint32_t* sj = si + kTail;                 // slot of position J[i]
+    uint32_t* lst = sj + kTail;                // two survivor lists (local ids)
+    uint32_t* cnt = lst + 2 * kTail;           // [0..1] list counters
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    for (uint32_t h = tid; h < kTab; h += blockDim.x) keys[h] = kEmpty;
+    if (tid < 2) cnt[tid] = 0;
+    __syncthreads();
+    for (uint32_t t = tid; t < n; t += blockDim.x) {
+        const uint2 v = __ldcg(cur + t);
+        const uint32_t i = v.x, j = v.y;
+        sidx[t] = i;
+        si[t] = tab_slot(keys, aval, a.A, i);
+        sj[t] = tab_slot(keys, aval, a.A, j);
+        lst[t] = t;
+    }
+    __syncthreads();
+    uint32_t which = 0;
+    while (n > 0 && round < kMaxRounds) {
+        const uint32_t* in = lst + which * kTail;
+        uint32_t* out = lst + (which ^ 1) * kTail;
+        for (uint32_t q = tid; q < n; q += blockDim.x) {
+            const uint32_t t = in[q];
+            rsv[si[t]] = kEmpty;
+            rsv[sj[t]] = kEmpty;
+        }
+        if (tid == 0) cnt[which ^ 1] = 0;
+        __syncthreads();
+        for (uint32_t q = tid; q < n; q += blockDim.x) {
+            const uint32_t t = in[q];
+            atomicMin(&rsv[si[t]], sidx[t]);
+            atomicMin(&rsv[sj[t]], sidx[t]);
+        }
+        __syncthreads();
+        for (uint32_t qb = tid - lane; qb < n; qb += blockDim.x) {
+            const uint32_t q = qb + lane;
+            bool pend = false;
+            uint32_t t = 0;
+            if (q < n) {
+                t = in[q];
+                const uint32_t x = si[t], y = sj[t], i = sidx[t];
+                if (rsv[x] == i && rsv[y] == i) {
+                    const uint32_t v = aval[x];
+                    aval[x] = aval[y];
+                    aval[y] = v;
                 } else {
                     pend = true;
                 }
             }
+            const unsigned mask = __ballot_sync(0xffffffffu, pend);
+            if (mask) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&cnt[which ^ 1], __popc(mask));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (pend) out[base + __popc(mask & ((1u << lane) - 1u))] = t;
+            }
         }
-        const unsigned mask = __ballot_sync(0xffffffffu, pend);
-        if (mask) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(next_cnt, __popc(mask));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (pend) next[base + __popc(mask & ((1u << lane) - 1u))] = i;
-        }
+        __syncthreads();
+        n = cnt[which ^ 1];
+        which ^= 1;
+        ++round;
+        __syncthreads();
     }
-    sync();
-    return ldcg(next_cnt);
+    for (uint32_t h = tid; h < kTab; h += blockDim.x)
+        if (keys[h] != kEmpty) a.A[keys[h]] = aval[h];
+    if (tid == 0) a.ctl[3] = n;  // non-zero only if the round guard tripped
+    return round;
 }
 
 __global__ void __launch_bounds__(kThreads) k_permute(PermArgs a) {
@@ -131,6 +275,9 @@ __global__ void __launch_bounds__(kThreads) k_permute(PermArgs a) {
     const uint32_t d = a.d;
     const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t nth = gridDim.x * blockDim.x;
+    // phase timestamps (globaltimer ns) for ll_last_permute_profile
+    uint64_t* ts = reinterpret_cast<uint64_t*>(a.ctl + 16);
+    if (gtid == 0) ts[0] = gtimer();
 
     // K2: identity, reservations cleared, all draws with shift 0.
     for (uint32_t i = gtid; i < d; i += nth) {
@@ -167,33 +314,52 @@ __global__ void __launch_bounds__(kThreads) k_permute(PermArgs a) {
         }
     }
 
-    // K3: deterministic-reservation rounds over the whole grid.
-    const uint32_t* cur = nullptr;
+    if (gtid == 0) ts[1] = gtimer();
+    // K3: deterministic-reservation rounds over the whole grid ...
+    const uint2* cur = nullptr;
     uint32_t n = d;
     uint32_t round = 1;
-    auto gsync = [&] { grid.sync(); };
-    while (n > kSmallList && round < kMaxRounds) {
-        uint32_t* next = (cur == a.L0) ? a.L1 : a.L0;
+    while (n > kTail && round < kMaxRounds) {
+        uint2* next = (cur == a.L0) ? a.L1 : a.L0;
         unsigned int* cnt = &a.ctl[4 + round % 3];
         if (gtid == 0) a.ctl[4 + (round + 1) % 3] = 0;
-        n = run_round(a, cur, n, next, cnt, round, gtid, nth, gsync);
+        n = run_round(a, cur, n, next, cnt, round, gtid, nth, grid);
         cur = next;
         ++round;
     }
     if (blockIdx.x != 0) return;
-    // Tail rounds inside CTA 0 (all grid writes are visible after grid.sync).
-    auto bsync = [] { __syncthreads(); };
-    while (n > 0 && round < kMaxRounds) {
-        uint32_t* next = (cur == a.L0) ? a.L1 : a.L0;
-        unsigned int* cnt = &a.ctl[4 + round % 3];
-        if (threadIdx.x == 0) a.ctl[4 + (round + 1) % 3] = 0;
-        n = run_round(a, cur, n, next, cnt, round, threadIdx.x, blockDim.x, bsync);
-        cur = next;
-        ++round;
+    if (threadIdx.x == 0) {
+        ts[2] = gtimer();
+        a.ctl[12] = round - 1;  // grid-wide rounds
     }
+    // ... then the tail in CTA 0's shared memory (grid writes are visible after
+    // the last grid.sync).  The first round may still run over the identity
+    // list when d itself is small.
+    if (n > 0 && cur == nullptr) {
+        // d <= kTail: materialise the identity survivor list (no-op swaps dropped)
+        uint2* next = a.L0;
+        if (threadIdx.x == 0) a.ctl[4] = 0;
+        __syncthreads();
+        for (uint32_t tb = threadIdx.x - (threadIdx.x & 31); tb < n; tb += blockDim.x) {
+            const uint32_t t = tb + (threadIdx.x & 31);
+            const uint32_t jt = t < n ? ldcg(a.J + t) : t;
+            const bool keep = t < n && jt != t;
+            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+            if (mask) {
+                uint32_t base = 0;
+                if ((threadIdx.x & 31) == 0) base = atomicAdd(&a.ctl[4], __popc(mask));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (keep) next[base + __popc(mask & ((1u << (threadIdx.x & 31)) - 1u))] = make_uint2(t, jt);
+            }
+        }
+        __syncthreads();
+        n = ldcg(&a.ctl[4]);
+        cur = next;
+    }
+    round = smem_tail(a, cur, n, round);
     if (threadIdx.x == 0) {
         a.ctl[2] = round - 1;
-        a.ctl[3] = n;  // survivors left: non-zero only if the round guard tripped
+        ts[3] = gtimer();
     }
 }
 
@@ -209,9 +375,9 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
                     const uint64_t* host_forced, uint64_t n_forced) {
     DevBuf& J = ctx->buf("perm.J", sizeof(uint32_t) * d);
     DevBuf& R = ctx->buf("perm.R", sizeof(unsigned long long) * d);
-    DevBuf& L0 = ctx->buf("perm.L0", sizeof(uint32_t) * d);
-    DevBuf& L1 = ctx->buf("perm.L1", sizeof(uint32_t) * d);
-    DevBuf& ctl = ctx->buf("perm.ctl", 64);
+    DevBuf& L0 = ctx->buf("perm.L0", sizeof(uint2) * d);
+    DevBuf& L1 = ctx->buf("perm.L1", sizeof(uint2) * d);
+    DevBuf& ctl = ctx->buf("perm.ctl", 128);
     unsigned int init[16] = {kNone, kNone, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     LL_CUDA(cudaMemcpyAsync(ctl.ptr, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
     PermArgs a{};
@@ -220,8 +386,8 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
     a.A = d_order;
     a.J = J.as<uint32_t>();
     a.R = R.as<unsigned long long>();
-    a.L0 = L0.as<uint32_t>();
-    a.L1 = L1.as<uint32_t>();
+    a.L0 = L0.as<uint2>();
+    a.L1 = L1.as<uint2>();
     a.ctl = ctl.as<unsigned int>();
     a.shift = reinterpret_cast<unsigned long long*>(ctl.as<unsigned int>() + 8);
     a.n_forced = static_cast<uint32_t>(n_forced);
@@ -232,8 +398,14 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
         LL_CUDA(cudaStreamSynchronize(ctx->stream));  // host_forced may be pageable
         a.forced = forced.as<uint64_t>();
     }
+    static bool attr = false;
+    if (!attr) {
+        LL_CUDA(cudaFuncSetAttribute(k_permute, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(kTailSmem)));
+        attr = true;
+    }
     int per_sm = 0;
-    LL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_permute, kThreads, 0));
+    LL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_permute, kThreads, kTailSmem));
     if (per_sm < 1) fail(LL_ERR_CUDA, "permute: kernel cannot be resident");
     const uint64_t want = (static_cast<uint64_t>(d) + kThreads - 1) / kThreads;
     const uint64_t cap = static_cast<uint64_t>(per_sm) * ctx->sm_count;
@@ -241,13 +413,13 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
     void* args[] = {&a};
     launch(ctx, "permute", [&] {
         LL_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_permute), dim3(grid),
-                                            dim3(kThreads), args, 0, ctx->stream));
+                                            dim3(kThreads), args, kTailSmem, ctx->stream));
     });
 }
 
 uint32_t permute_rounds(ll_ctx* ctx) {
     unsigned int ctl[2] = {0, 0};
-    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf("perm.ctl", 64).as<unsigned int>() + 2, sizeof(ctl),
+    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf("perm.ctl", 128).as<unsigned int>() + 2, sizeof(ctl),
                             cudaMemcpyDeviceToHost, ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctl[1] != 0) fail(LL_ERR_RUNTIME, "permute: round limit exceeded (internal error)");
@@ -257,6 +429,21 @@ uint32_t permute_rounds(ll_ctx* ctx) {
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n) {
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 148u * 8u));
     launch(ctx, "widen", [&] { k_widen<<<grid ? grid : 1, 256, 0, ctx->stream>>>(in, out, n); });
+}
+
+// {rounds, grid-wide rounds, ns draws+repair, ns grid rounds, ns CTA-0 rounds, ns total}
+void permute_profile(ll_ctx* ctx, uint64_t* out6) {
+    unsigned int ctl[32];
+    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf("perm.ctl", 128).ptr, sizeof(ctl),
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    LL_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint64_t* ts = reinterpret_cast<const uint64_t*>(ctl + 16);
+    out6[0] = ctl[2];
+    out6[1] = ctl[12];
+    out6[2] = ts[1] - ts[0];
+    out6[3] = ts[2] - ts[1];
+    out6[4] = ts[3] - ts[2];
+    out6[5] = ts[3] - ts[0];
 }
 
 } // namespace ll
