@@ -40,6 +40,7 @@ enum { LL_SCHEME_REGULAR = 0, LL_SCHEME_LOCALITY = 1, LL_SCHEME_LOCALITY_BALANCE
 enum { LL_EXCHANGE_NONE = 0, LL_EXCHANGE_NCCL = 1, LL_EXCHANGE_P2P = 2 };
 enum { LL_OUT_F32 = 0, LL_OUT_BF16 = 1 };
 enum { LL_AUG_CROP = 0, LL_AUG_RESIZE = 1 };
+enum { LL_GEOM_FIXED = 0, LL_GEOM_VARIABLE = 1 };
 
 typedef struct ll_ctx ll_ctx;       /* one CUDA device + stream + workspace   */
 typedef struct ll_loader ll_loader; /* one learner's HBM shard + epoch plan   */
@@ -170,7 +171,11 @@ typedef struct ll_loader_config {
     int32_t scheme;           /* LL_SCHEME_*                                     */
     int32_t exchange;         /* LL_EXCHANGE_*                                   */
     uint32_t prefetch_depth;  /* LoaderConfig::prefetch_depth: output ring depth */
-    uint32_t reserved;
+    uint32_t geometry;        /* LL_GEOM_FIXED: every sample height x width;
+                                 LL_GEOM_VARIABLE: sample id is H x W with
+                                 H, W = 128 + bounded(385) from
+                                 SplitMix64(derive_seed(data_seed, id, 1))
+                                 (cfg5; needs augment.mode = LL_AUG_RESIZE) */
     ll_augment_spec augment;
 } ll_loader_config;
 

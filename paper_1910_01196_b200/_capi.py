@@ -16,6 +16,7 @@ SCHEME_REGULAR, SCHEME_LOCALITY, SCHEME_LOCALITY_BALANCED = 0, 1, 2
 EXCHANGE_NONE, EXCHANGE_NCCL, EXCHANGE_P2P = 0, 1, 2
 OUT_F32, OUT_BF16 = 0, 1
 AUG_CROP, AUG_RESIZE = 0, 1
+GEOM_FIXED, GEOM_VARIABLE = 0, 1
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)
@@ -39,7 +40,7 @@ class LoaderConfig(C.Structure):
                 ("learners", C.c_uint32), ("rank", C.c_uint32), ("batch_size", C.c_uint64),
                 ("alpha", C.c_double), ("seed", C.c_uint64), ("data_seed", C.c_uint64),
                 ("scheme", C.c_int32), ("exchange", C.c_int32), ("prefetch_depth", C.c_uint32),
-                ("reserved", C.c_uint32), ("augment", AugmentSpec)]
+                ("geometry", C.c_uint32), ("augment", AugmentSpec)]
 
 
 class StepInfo(C.Structure):

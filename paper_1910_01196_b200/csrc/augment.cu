@@ -17,10 +17,12 @@
 // PX consecutive output pixels of all three planes as 128-bit streaming
 // stores, so every warp writes 512 contiguous bytes per plane row.
 #include "ll_internal.h"
+#include "geometry.cuh"
 #include "locload_rng.cuh"
 
 #include <cuda_bf16.h>
 
+#include <cmath>
 #include <cstdlib>
 
 namespace ll {
@@ -69,11 +71,12 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
     const uint64_t s = list[k];
     *id = s;
     if (k < kept) {
-        *src = m.shard + (s - m.shard_first) * m.sample_bytes;
+        *src = m.shard + (m.prefix ? m.prefix[s] - m.prefix[m.shard_first]
+                                   : (s - m.shard_first) * m.sample_bytes);
     } else if (m.peers) {
         const uint32_t o = static_cast<uint32_t>(s * m.p / m.cached);
         const uint64_t first = (static_cast<uint64_t>(o) * m.cached + m.p - 1) / m.p;
-        *src = m.peers[o] + (s - first) * m.sample_bytes;
+        *src = m.peers[o] + (m.prefix ? m.prefix[s] - m.prefix[first] : (s - first) * m.sample_bytes);
     } else {
         *src = m.recv + (k - kept) * m.sample_bytes;
     }
@@ -340,6 +343,123 @@ __global__ void __launch_bounds__(256) k_augment_resize(AugArgs a) {
     }
 }
 
+// K7 banded: one CTA per (sample, kRB output rows).  The source rows those
+// output rows tap (crop-window columns only, 16-byte aligned chunks) are
+// staged in shared memory once; per-column taps (xlo, xhi, wx) are tabled
+// once per CTA; each thread then emits pixel pairs of all three planes.  The
+// per-sample geometry comes from the id (cfg5) or the launch (fixed).
+constexpr uint32_t kRB = 8;
+constexpr uint32_t kMaxOutW = 512;
+
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_augment_resize_band(AugArgs a, uint32_t max_rows,
+                                                             uint32_t row_stride) {
+    extern __shared__ __align__(16) uint8_t rowbuf[];  // [max_rows][row_stride]
+    __shared__ float s_wx[kMaxOutW];
+    __shared__ uint16_t s_xlo[kMaxOutW], s_xhi[kMaxOutW];
+    __shared__ uint32_t s_shift[64];
+    __shared__ const uint8_t* s_src;
+    __shared__ Params s_prm;
+    __shared__ uint32_t s_W;
+    const uint32_t bands = (a.out_h + kRB - 1) / kRB;
+    const uint64_t k = blockIdx.x / bands;
+    const uint32_t oy0 = (blockIdx.x - static_cast<uint32_t>(k) * bands) * kRB;
+    const uint32_t rows_out = a.out_h - oy0 < kRB ? a.out_h - oy0 : kRB;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        uint64_t id;
+        const uint8_t* src;
+        resolve(a.src, k, &id, &src);
+        uint32_t H = a.H, W = a.W;
+        if (a.src.prefix) var_hw(a.src.data_seed, id, &H, &W);
+        s_src = src;
+        s_W = W;
+        s_prm = aug_params(a.seed, a.epoch, id, H, W, a.out_h, a.out_w, LL_AUG_RESIZE);
+    }
+    __syncthreads();
+    const Params q = s_prm;
+    const uint32_t W = s_W;
+    const float sy = __fdiv_rn(static_cast<float>(q.ch), static_cast<float>(a.out_h));
+    const float sx = __fdiv_rn(static_cast<float>(q.cw), static_cast<float>(a.out_w));
+    // column taps (the oracle's exact op sequence)
+    for (uint32_t ox = tid; ox < a.out_w; ox += blockDim.x) {
+        const uint32_t mx = q.flip ? a.out_w - 1 - ox : ox;
+        float fx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(mx), 0.5f), sx), 0.5f);
+        if (fx < 0.f) fx = 0.f;
+        uint32_t xlo = static_cast<uint32_t>(fx);
+        if (xlo > q.cw - 1) xlo = q.cw - 1;
+        s_xlo[ox] = static_cast<uint16_t>(xlo);
+        s_xhi[ox] = static_cast<uint16_t>(xlo + 1 < q.cw ? xlo + 1 : q.cw - 1);
+        s_wx[ox] = __fsub_rn(fx, static_cast<float>(xlo));
+    }
+    auto tap_y = [&](uint32_t oy, uint32_t* lo, uint32_t* hi, float* w) {
+        float fy = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(oy), 0.5f), sy), 0.5f);
+        if (fy < 0.f) fy = 0.f;
+        uint32_t ylo = static_cast<uint32_t>(fy);
+        if (ylo > q.ch - 1) ylo = q.ch - 1;
+        *lo = ylo;
+        *hi = ylo + 1 < q.ch ? ylo + 1 : q.ch - 1;
+        *w = __fsub_rn(fy, static_cast<float>(ylo));
+    };
+    uint32_t r_first, r_last, t0;
+    float tw;
+    tap_y(oy0, &r_first, &t0, &tw);
+    tap_y(oy0 + rows_out - 1, &t0, &r_last, &tw);
+    const uint32_t nrows = r_last - r_first + 1;  // <= max_rows (host bound)
+    // stage the tapped source rows: bytes [x0*3, (x0+cw)*3) of each, 16-B aligned
+    const uint32_t nchunk = row_stride / 16;
+    for (uint32_t r = tid; r < nrows; r += blockDim.x) {
+        const uintptr_t g = reinterpret_cast<uintptr_t>(s_src) +
+                            static_cast<uint64_t>(q.y0 + r_first + r) * W * 3 + q.x0 * 3;
+        s_shift[r] = static_cast<uint32_t>(g & 15);
+    }
+    __syncthreads();
+    for (uint32_t t = tid; t < nrows * nchunk; t += blockDim.x) {
+        const uint32_t r = t / nchunk, c = t - r * nchunk;
+        const uintptr_t g = reinterpret_cast<uintptr_t>(s_src) +
+                            static_cast<uint64_t>(q.y0 + r_first + r) * W * 3 + q.x0 * 3;
+        const uintptr_t a16 = g & ~static_cast<uintptr_t>(15);
+        if (a16 + 16 * c < g + 3ull * q.cw)
+            *reinterpret_cast<uint4*>(rowbuf + r * row_stride + 16 * c) =
+                ld_nc_v4(reinterpret_cast<const void*>(a16 + 16 * c));
+    }
+    __syncthreads();
+    const uint64_t plane = static_cast<uint64_t>(a.out_h) * a.out_w;
+    const uint32_t pairs = a.out_w / 2;
+    for (uint32_t task = tid; task < rows_out * pairs; task += blockDim.x) {
+        const uint32_t rr = task / pairs, ox = 2 * (task - rr * pairs), oy = oy0 + rr;
+        uint32_t ylo, yhi;
+        float wy;
+        tap_y(oy, &ylo, &yhi, &wy);
+        const uint8_t* r0 = rowbuf + (ylo - r_first) * row_stride + s_shift[ylo - r_first];
+        const uint8_t* r1 = rowbuf + (yhi - r_first) * row_stride + s_shift[yhi - r_first];
+        float o[3][2];
+#pragma unroll
+        for (uint32_t e = 0; e < 2; ++e) {
+            const uint32_t pa = 3u * s_xlo[ox + e], pb = 3u * s_xhi[ox + e];
+            const float wx = s_wx[ox + e];
+#pragma unroll
+            for (uint32_t c = 0; c < 3; ++c) {
+                const float p00 = r0[pa + c], p01 = r0[pb + c], p10 = r1[pa + c], p11 = r1[pb + c];
+                const float top = __fadd_rn(p00, __fmul_rn(wx, __fsub_rn(p01, p00)));
+                const float bot = __fadd_rn(p10, __fmul_rn(wx, __fsub_rn(p11, p10)));
+                const float v = __fadd_rn(top, __fmul_rn(wy, __fsub_rn(bot, top)));
+                o[c][e] = __fmul_rn(__fsub_rn(v, a.nc.mean255[c]), a.nc.inv_std255[c]);
+            }
+        }
+#pragma unroll
+        for (uint32_t c = 0; c < 3; ++c) {
+            const uint64_t idx = k * 3 * plane + c * plane + static_cast<uint64_t>(oy) * a.out_w + ox;
+            if constexpr (BF16) {
+                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(a.out) + idx) =
+                    __floats2bfloat162_rn(o[c][0], o[c][1]);
+            } else {
+                *reinterpret_cast<float2*>(static_cast<float*>(a.out) + idx) = make_float2(o[c][0], o[c][1]);
+            }
+        }
+    }
+}
+
 __global__ void k_aug_params(uint64_t seed, uint64_t epoch, const uint64_t* __restrict__ ids,
                              uint64_t n, uint32_t H, uint32_t W, uint32_t out_h, uint32_t out_w,
                              int mode, uint32_t* __restrict__ out5) {
@@ -421,6 +541,32 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
                 k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);
         });
     } else {
+        // banded kernel when its staged rows fit in shared memory
+        const uint32_t max_side = src.prefix ? kVarMin + kVarSpan - 1 : (height < width ? height : width);
+        const double scale = static_cast<double>(max_side) / spec.out_h;
+        const uint32_t max_rows = static_cast<uint32_t>(std::ceil(kRB * scale)) + 3;
+        const uint32_t max_w = src.prefix ? kVarMin + kVarSpan - 1 : width;
+        const uint32_t row_stride = ((3 * max_w + 15) / 16 + 1) * 16;
+        const size_t smem = static_cast<size_t>(max_rows) * row_stride;
+        if (spec.out_w % 2 == 0 && spec.out_w <= kMaxOutW && max_rows <= 64 && smem <= 160 * 1024) {
+            static bool attr = false;
+            if (!attr) {
+                LL_CUDA(cudaFuncSetAttribute(k_augment_resize_band<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+                LL_CUDA(cudaFuncSetAttribute(k_augment_resize_band<true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+                attr = true;
+            }
+            const dim3 grid(static_cast<unsigned>(n * ((spec.out_h + kRB - 1) / kRB)));
+            launch(ctx, "augment_resize", [&] {
+                if (bf16)
+                    k_augment_resize_band<true><<<grid, 256, smem, ctx->stream>>>(a, max_rows, row_stride);
+                else
+                    k_augment_resize_band<false><<<grid, 256, smem, ctx->stream>>>(a, max_rows, row_stride);
+            });
+            return;
+        }
+        require(src.prefix == nullptr, "augment: variable geometry needs the banded resize kernel");
         const dim3 grid(static_cast<unsigned>(n * spec.out_h));
         launch(ctx, "augment_resize", [&] {
             if (bf16)

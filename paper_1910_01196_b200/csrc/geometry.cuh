@@ -1,0 +1,25 @@
+// geometry.cuh -- per-sample source geometry of the variable-size dataset
+// (BASELINE configs[4], cfg5): sample id is H x W x 3 u8 HWC with
+// H, W = 128 + bounded(385) drawn from SplitMix64(derive_seed(data_seed, id, 1))
+// (oracle: lo_sample_hw).  Samples are stored back to back, each padded to 16
+// bytes; every learner computes the same global prefix of padded sizes, so a
+// sample's offset inside its owner's shard is prefix[s] - prefix[first(owner)].
+#pragma once
+#include <cstdint>
+
+#include "locload_rng.cuh"
+
+namespace ll {
+
+constexpr uint32_t kVarMin = 128;
+constexpr uint32_t kVarSpan = 385;  // H, W in [128, 512]
+
+LL_HD void var_hw(uint64_t data_seed, uint64_t id, uint32_t* h, uint32_t* w) {
+    SplitMix r(derive_seed(data_seed, id, 1));
+    *h = kVarMin + static_cast<uint32_t>(r.bounded(kVarSpan));
+    *w = kVarMin + static_cast<uint32_t>(r.bounded(kVarSpan));
+}
+
+LL_HD uint64_t pad16(uint64_t b) { return (b + 15) & ~15ull; }
+
+} // namespace ll

@@ -144,6 +144,10 @@ void generate_range_device(ll_ctx* ctx, uint8_t* dst, uint64_t first_id, uint64_
                            uint64_t sample_bytes, uint64_t data_seed);
 void generate_ids_device(ll_ctx* ctx, uint8_t* dst, const uint64_t* d_ids, uint64_t n,
                          uint64_t sample_bytes, uint64_t data_seed);
+// variable geometry (geometry.cuh): d_prefix[0..d] = exclusive prefix of padded sizes
+void var_prefix_device(ll_ctx* ctx, uint64_t* d_prefix, uint64_t d, uint64_t data_seed);
+void generate_var_device(ll_ctx* ctx, uint8_t* shard, uint64_t first, uint64_t n,
+                         const uint64_t* d_prefix, uint64_t data_seed);
 
 // augment.cu
 struct NormConst {
@@ -171,6 +175,10 @@ struct SrcMap {
     uint32_t p = 1;
     uint64_t cached = 0;
     uint64_t sample_bytes = 0;
+    // variable geometry (cfg5): offsets from the global padded-size prefix,
+    // geometry from the id (geometry.cuh); recv/explicit paths need fixed size
+    const uint64_t* prefix = nullptr;
+    uint64_t data_seed = 0;
 };
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
                     const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out);

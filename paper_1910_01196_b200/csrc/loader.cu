@@ -20,6 +20,7 @@
 #include <cstring>
 #include <vector>
 
+#include "geometry.cuh"
 #include "ll_internal.h"
 
 namespace ll {
@@ -45,6 +46,8 @@ struct ll_loader {
     uint64_t max_local = 0;
     ll::DevBuf shard;
     bool populated = false;
+    ll::DevBuf prefix;            // variable geometry: global padded-size prefix [d+1]
+    std::vector<uint64_t> h_prefix_ends;  // prefix at first and first+owned
     // epoch plan
     ll::DevBuf order;
     ll::PlanBufs plan;
@@ -147,6 +150,10 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     src.p = p;
     src.cached = ld->cached;
     src.sample_bytes = ld->S;
+    if (c.geometry == LL_GEOM_VARIABLE) {
+        src.prefix = ld->prefix.as<uint64_t>();
+        src.data_seed = c.data_seed;
+    }
     if (c.augment.mode == LL_AUG_CROP) src.aug = pd.aug + step * B + h_off[me];
     if (p > 1 && c.scheme == LL_SCHEME_REGULAR) {
         // reg_slice (sampling.cpp:27-42) ignores ownership: every sample of the
@@ -159,6 +166,8 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     } else if (p > 1 && (n_send || n_recv)) {
         if (c.exchange == LL_EXCHANGE_NCCL) {
             require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
+            require(c.geometry == LL_GEOM_FIXED,
+                    "loader: variable-size samples need the P2P exchange");
             const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
             ld->packbuf.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
             ld->recvbuf.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
@@ -187,7 +196,9 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     ensure_out(ld);
     void* out = ld->out[ld->out_slot]->ptr;
     ld->out_slot = (ld->out_slot + 1) % ld->out.size();
-    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, c.height, c.width, out);
+    const uint32_t gh = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.height;
+    const uint32_t gw = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.width;
+    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, gh, gw, out);
     if (info) {
         info->epoch = epoch;
         info->step = step;
@@ -218,7 +229,8 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
     require(c.learners <= kMaxP, "Loader: at most 64 learners per box");
     require(c.rank < c.learners, "Loader: rank out of range");
     require(c.d < 0xFFFFFFFFull, "Loader: dataset size must be < 2^32 - 1 on the device");
-    require(c.height >= 1 && c.width >= 1, "Loader: empty sample geometry");
+    require(c.geometry == LL_GEOM_VARIABLE || (c.height >= 1 && c.width >= 1),
+            "Loader: empty sample geometry");
     require(c.scheme >= LL_SCHEME_REGULAR && c.scheme <= LL_SCHEME_LOCALITY_BALANCED,
             "Loader: unknown scheme");
     if (c.scheme == LL_SCHEME_REGULAR)
@@ -227,7 +239,12 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
     auto ld = std::make_unique<ll_loader>();
     ld->ctx = ctx;
     ld->cfg = c;
-    ld->S = static_cast<uint64_t>(c.height) * c.width * 3;
+    require(c.geometry == LL_GEOM_FIXED || c.geometry == LL_GEOM_VARIABLE,
+            "Loader: unknown geometry");
+    if (c.geometry == LL_GEOM_VARIABLE)
+        require(c.augment.mode == LL_AUG_RESIZE,
+                "Loader: variable-size samples need augment.mode = LL_AUG_RESIZE");
+    ld->S = c.geometry == LL_GEOM_FIXED ? static_cast<uint64_t>(c.height) * c.width * 3 : 0;
     ld->cached = static_cast<uint64_t>(c.alpha * static_cast<double>(c.d));  // sampling.cpp:15
     if (ld->cached > c.d) ld->cached = c.d;
     require(ld->cached >= 1, "Loader: alpha * d must cache at least one sample");
@@ -239,7 +256,21 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
     ld->max_local = c.scheme == LL_SCHEME_LOCALITY ? c.batch_size
                                                    : (c.batch_size + p - 1) / p;
     set_device(ctx);
-    ld->shard.reserve(std::max<uint64_t>(ld->owned * ld->S, 16));
+    uint64_t shard_bytes = ld->owned * ld->S;
+    if (c.geometry == LL_GEOM_VARIABLE) {
+        // every learner computes the same global prefix of padded sample sizes
+        ld->prefix.reserve(sizeof(uint64_t) * (c.d + 1));
+        var_prefix_device(ctx, ld->prefix.as<uint64_t>(), c.d, c.data_seed);
+        uint64_t ends[2];
+        LL_CUDA(cudaMemcpyAsync(&ends[0], ld->prefix.as<uint64_t>() + ld->first, 8,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        LL_CUDA(cudaMemcpyAsync(&ends[1], ld->prefix.as<uint64_t>() + ld->first + ld->owned, 8,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        LL_CUDA(cudaStreamSynchronize(ctx->stream));
+        ld->h_prefix_ends.assign(ends, ends + 2);
+        shard_bytes = ends[1] - ends[0];
+    }
+    ld->shard.reserve(std::max<uint64_t>(shard_bytes, 16));
     ld->order.reserve(sizeof(uint32_t) * c.d);
     ld->plan.reserve(ld->steps, c.batch_size);
     *out = ld.release();
@@ -312,7 +343,11 @@ void loader_link_peers(ll_loader* const* lds, uint32_t n) {
 
 void loader_populate(ll_loader* ld) {
     set_device(ld->ctx);
-    generate_range_device(ld->ctx, ld->shard.as<uint8_t>(), ld->first, ld->owned, ld->S,
+    if (ld->cfg.geometry == LL_GEOM_VARIABLE)
+        generate_var_device(ld->ctx, ld->shard.as<uint8_t>(), ld->first, ld->owned,
+                            ld->prefix.as<uint64_t>(), ld->cfg.data_seed);
+    else
+        generate_range_device(ld->ctx, ld->shard.as<uint8_t>(), ld->first, ld->owned, ld->S,
                           ld->cfg.data_seed);
     LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));
     ld->populated = true;
@@ -320,6 +355,8 @@ void loader_populate(ll_loader* ld) {
 
 void loader_populate_from_host(ll_loader* ld, const uint8_t* host) {
     set_device(ld->ctx);
+    require(ld->cfg.geometry == LL_GEOM_FIXED,
+            "Loader: populate_from_host supports fixed-size samples");
     LL_CUDA(cudaMemcpyAsync(ld->shard.ptr, host, ld->owned * ld->S, cudaMemcpyHostToDevice,
                             ld->ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));

@@ -5,7 +5,10 @@
 // SplitMix64(derive_seed(seed, id)).  Because the stream is counter based,
 // every 16-byte chunk (draws 2c, 2c+1) is independent: one thread writes one
 // 128-bit chunk with a streaming store.  Write-bound: HBM roofline.
+#include <algorithm>
+
 #include "ll_internal.h"
+#include "geometry.cuh"
 #include "locload_rng.cuh"
 
 namespace ll {
@@ -61,7 +64,74 @@ void run(ll_ctx* ctx, uint8_t* dst, uint64_t first_id, const uint64_t* ids, uint
     });
 }
 
+// Variable geometry: padded byte size of every id in [0, d) into vals[0..d).
+__global__ void k_var_sizes(uint64_t* __restrict__ vals, uint64_t d, uint64_t data_seed) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < d;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint32_t h, w;
+        var_hw(data_seed, i, &h, &w);
+        vals[i] = pad16(3ull * h * w);
+    }
+}
+
+// In-place exclusive scan of vals[0..n) into vals[0..n], one CTA (setup only:
+// run once per loader).  Thread t owns a contiguous chunk.
+__global__ void __launch_bounds__(1024) k_scan1(uint64_t* vals, uint64_t n) {
+    __shared__ uint64_t part[1024];
+    const uint64_t chunk = (n + blockDim.x - 1) / blockDim.x;
+    const uint64_t b = threadIdx.x * chunk, e = b + chunk < n ? b + chunk : n;
+    uint64_t sum = 0;
+    for (uint64_t i = b; i < e; ++i) sum += vals[i];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (uint32_t off = 1; off < blockDim.x; off <<= 1) {
+        const uint64_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint64_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+    for (uint64_t i = b; i < e; ++i) {
+        const uint64_t v = vals[i];
+        vals[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == blockDim.x - 1) vals[n] = part[blockDim.x - 1];
+}
+
+// One CTA per owned sample: the generate_dataset bytes of sample first+t at
+// shard + prefix[first+t] - prefix[first].
+__global__ void __launch_bounds__(256) k_generate_var(uint8_t* __restrict__ shard, uint64_t first,
+                                                      const uint64_t* __restrict__ prefix,
+                                                      uint64_t data_seed) {
+    const uint64_t id = first + blockIdx.x;
+    uint32_t h, w;
+    var_hw(data_seed, id, &h, &w);
+    const uint64_t bytes = 3ull * h * w;
+    uint8_t* dst = shard + (prefix[id] - prefix[first]);
+    const uint64_t key = derive_seed(data_seed, id);
+    for (uint64_t c = threadIdx.x; c < (bytes + 15) / 16; c += blockDim.x)
+        gen_chunk(dst, key, c, bytes, true);
+}
+
 } // namespace
+
+void var_prefix_device(ll_ctx* ctx, uint64_t* d_prefix, uint64_t d, uint64_t data_seed) {
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((d + 255) / 256, 148u * 8u));
+    launch(ctx, "var_sizes", [&] {
+        k_var_sizes<<<grid ? grid : 1, 256, 0, ctx->stream>>>(d_prefix, d, data_seed);
+    });
+    launch(ctx, "scan", [&] { k_scan1<<<1, 1024, 0, ctx->stream>>>(d_prefix, d); });
+}
+
+void generate_var_device(ll_ctx* ctx, uint8_t* shard, uint64_t first, uint64_t n,
+                         const uint64_t* d_prefix, uint64_t data_seed) {
+    if (n == 0) return;
+    launch(ctx, "generate", [&] {
+        k_generate_var<<<static_cast<unsigned>(n), 256, 0, ctx->stream>>>(shard, first, d_prefix,
+                                                                         data_seed);
+    });
+}
 
 void generate_range_device(ll_ctx* ctx, uint8_t* dst, uint64_t first_id, uint64_t n,
                            uint64_t sample_bytes, uint64_t data_seed) {

@@ -58,6 +58,7 @@ class LoaderConfig:
     scheme: str = "locality_balanced"
     exchange: str = "none"         # "none" | "nccl" | "p2p"
     prefetch_depth: int = 2
+    geometry: str = "fixed"        # "fixed" (height x width) | "variable" (cfg5, 128-512 px)
     augment: AugmentConfig = field(default_factory=AugmentConfig)
 
     def to_c(self) -> _capi.LoaderConfig:
@@ -68,6 +69,7 @@ class LoaderConfig:
         c.scheme = {"regular": 0, "locality": 1, "locality_balanced": 2}[self.scheme]
         c.exchange = {"none": 0, "nccl": 1, "p2p": 2}[self.exchange]
         c.prefetch_depth = self.prefetch_depth
+        c.geometry = {"fixed": 0, "variable": 1}[self.geometry]
         c.augment = self.augment.to_c()
         return c
 

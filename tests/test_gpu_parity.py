@@ -450,3 +450,38 @@ def test_loader_config_errors():
     with pytest.raises(ValueError, match="exchange"):
         for t in range(10):
             ld.step(0, t)
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_loader_variable_size_resize_vs_oracle(dtype):
+    """cfg5: variable 128-512 px sources (geometry from the id), bilinear resize
+    to 224, two learners with P2P exchange; every delivered sample equals the
+    oracle's restatement bit for bit (tolerance 1 ulp bf16 / 1e-5 fp32)."""
+    d, p, B, seed = 3000, 2, 96, 42
+    lds = []
+    for j in range(p):
+        ld = DeviceLoader(LoaderConfig(d=d, height=0, width=0, learners=p, rank=j, batch_size=B,
+                                       seed=seed, data_seed=seed, exchange="p2p",
+                                       geometry="variable",
+                                       augment=AugmentConfig(mode="resize", out_dtype=dtype)))
+        ld.populate()
+        lds.append(ld)
+    DeviceLoader.link_peers(lds)
+    order = oracle.permute_epoch(seed, 2, d)
+    for t in [0, 9]:
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, d, oracle.MODE_LOCALITY_BALANCED)
+        for j, ld in enumerate(lds):
+            info = ld.step(2, t)
+            lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            got = ld.fetch(info)
+            for k, sid in enumerate(lst[:24]):
+                H, W = oracle.sample_hw(seed, int(sid))
+                src = oracle.gen_sample(seed, int(sid), H * W * 3).reshape(H, W, 3)
+                want = oracle.augment(src, int(sid), seed, 2, mode=oracle.AUG_RESIZE,
+                                      bf16=dtype == "bf16")
+                if dtype == "fp32":
+                    assert np.abs(got[k] - want).max() <= FP32_TOL
+                else:
+                    assert bf16_ulps(got[k], want) <= 1
+                assert np.array_equal(got[k], want), (t, j, k, H, W)
