@@ -49,21 +49,46 @@ def parse():
     ap.add_argument("--steps", type=int, default=1560)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
+                    help="cfg2: fixed 256x256 crop224 (default, the headline); "
+                         "cfg5: variable 128-512 px, bilinear resize to 224")
+    ap.add_argument("--dtype", default=None, choices=["fp32", "bf16"],
+                    help="output dtype (default fp32 for cfg2, bf16 for cfg5)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--per-gpu-d", type=int, default=PER_GPU_D)
     ap.add_argument("--per-gpu-batch", type=int, default=PER_GPU_B)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.dtype is None:
+        args.dtype = "bf16" if args.workload == "cfg5" else "fp32"
+    return args
+
+
+def mean_window_bytes_cfg5() -> float:
+    """E[3 * min(H, W)^2] for H, W iid uniform on [128, 512] (geometry.cuh):
+    the resize crop window (the source region an output depends on)."""
+    v = np.arange(128, 513, dtype=np.float64)
+    mn = np.minimum(v[:, None], v[None, :])
+    return float(3.0 * (mn ** 2).mean())
+
+
+def src_bytes_per_sample(args) -> float:
+    return mean_window_bytes_cfg5() if args.workload == "cfg5" else float(SRC_BYTES)
 
 
 def workload(args, n):
-    return {"workload": "cfg2-weak: ImageNet-1K-shaped synthetic u8 256x256x3, "
-                        f"d={args.per_gpu_d}*N, p=N, global batch {args.per_gpu_batch}*N, "
-                        "alpha=1, locality_balanced, crop224+flip+normalize -> NCHW "
-                        f"{args.dtype}",
+    if args.workload == "cfg5":
+        name = ("cfg5-weak: variable-size synthetic u8 HWC (H, W uniform 128-512 px), "
+                f"d={args.per_gpu_d}*N, p=N, global batch {args.per_gpu_batch}*N, alpha=1, "
+                f"locality_balanced, random square crop + flip + bilinear resize 224 + "
+                f"normalize -> NCHW {args.dtype}")
+    else:
+        name = ("cfg2-weak: ImageNet-1K-shaped synthetic u8 256x256x3, "
+                f"d={args.per_gpu_d}*N, p=N, global batch {args.per_gpu_batch}*N, "
+                f"alpha=1, locality_balanced, crop224+flip+normalize -> NCHW {args.dtype}")
+    return {"workload": name,
             "d": args.per_gpu_d * n, "learners": n, "global_batch": args.per_gpu_batch * n,
             "per_gpu_batch": args.per_gpu_batch, "alpha": 1.0, "scheme": "locality_balanced",
             "exchange": args.exchange if n > 1 else "none", "out_dtype": args.dtype,
@@ -138,7 +163,10 @@ def cpu_reference_run(args, n, steps, warmup, seconds_cap=None):
     d, B = args.per_gpu_d * n, args.per_gpu_batch * n
     spe = d // B
     pool_n = 4096
-    pool = np.stack([oracle.gen_sample(SEED, i, H * W * 3) for i in range(pool_n)])
+    if args.workload == "cfg5":
+        vpool = oracle.VarPool(SEED, pool_n)
+    else:
+        pool = np.stack([oracle.gen_sample(SEED, i, H * W * 3) for i in range(pool_n)])
     cores = len(os.sched_getaffinity(0))
     chunk = min(B, 1024)
     out = np.empty(chunk * out_bytes(args.dtype), np.uint8)
@@ -153,7 +181,10 @@ def cpu_reference_run(args, n, steps, warmup, seconds_cap=None):
         batch = cache["order"][s * B:(s + 1) * B]
         lists, off, _ = oracle.ref_assign_balanced(batch, d, n)    # sampling+balance
         for c0 in range(0, B, chunk):
-            oracle.cpu_crop_step(pool, lists[c0:c0 + chunk], H, W, SEED, e, out, bf16, cores)
+            if args.workload == "cfg5":
+                oracle.cpu_resize_step(vpool, lists[c0:c0 + chunk], SEED, e, out, bf16, cores)
+            else:
+                oracle.cpu_crop_step(pool, lists[c0:c0 + chunk], H, W, SEED, e, out, bf16, cores)
         return B
 
     for t in range(warmup):
@@ -169,6 +200,24 @@ def cpu_reference_run(args, n, steps, warmup, seconds_cap=None):
     dt = time.perf_counter() - t0
     return {"value": samples / dt, "unit": "samples/s", "cores": cores, "steps": done,
             "seconds": dt}
+
+
+def remote_summary(args, n, d, B, totals):
+    """Remote samples per epoch: locality-balanced moves (measured from the
+    device plan) vs the regular scheme's remote samples (counted in the same
+    plan) vs the paper's model, Eq. 7 (alpha*D*(p-1)/p) and Eq. 8
+    (alpha*D*beta) with beta measured as moved/B (model.hpp:65-74)."""
+    per = H * W * 3 if args.workload == "cfg2" else mean_window_bytes_cfg5() / 1.0
+    steps = d // B
+    beta = totals["moved"] / (steps * B) if steps else 0.0
+    return {"loc_moved_samples": totals["moved"],
+            "loc_nvlink_samples": totals["moved_nvlink"],
+            "reg_remote_samples": totals["reg_remote"],
+            "eq7_samples": d * (n - 1) / n, "eq8_samples": d * beta, "beta": beta,
+            "bytes_per_sample": per,
+            "loc_remote_bytes": totals["moved_nvlink"] * per,
+            "reg_remote_bytes": totals["reg_remote"] * per,
+            "local_fraction": 1.0 - (totals["moved"] / (steps * B) if steps else 0.0)}
 
 
 def run_reference(args):
@@ -210,10 +259,14 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     d, B = args.per_gpu_d * n, args.per_gpu_batch * n
+    cfg5 = args.workload == "cfg5"
     cfg = LoaderConfig(d=d, height=H, width=W, learners=n, rank=rank, batch_size=B, alpha=1.0,
                        seed=SEED, data_seed=SEED, scheme="locality_balanced",
                        exchange=args.exchange if n > 1 else "none", prefetch_depth=2,
-                       augment=AugmentConfig(out_dtype=args.dtype))
+                       geometry="variable" if cfg5 else "fixed",
+                       augment=AugmentConfig(mode="resize" if cfg5 else "crop",
+                                             out_dtype=args.dtype))
+    aug_kernel = "augment_resize" if cfg5 else "augment_crop"
     ld = DeviceLoader(cfg, device=local)
     ld.populate()                                   # K1: this learner's shard in HBM
     if n > 1:
@@ -291,12 +344,12 @@ def run_ours(args):
     barrier()
     _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     stats = {}
-    for name in ["augment_crop", "permute", "assign", "pack"]:
+    for name in [aug_kernel, "permute", "assign", "pack"]:
         cnt, tot = C.c_uint64(), C.c_double()
         _capi.check(lib.ll_ctx_kernel_stats(ctx, name.encode(), C.byref(cnt), C.byref(tot)))
         stats[name] = (cnt.value, tot.value)
-    aug_n, aug_ms = stats["augment_crop"]
-    per_launch_bytes = args.per_gpu_batch * (SRC_BYTES + out_bytes(args.dtype))
+    aug_n, aug_ms = stats[aug_kernel]
+    per_launch_bytes = args.per_gpu_batch * (src_bytes_per_sample(args) + out_bytes(args.dtype))
     achieved = per_launch_bytes / (aug_ms / aug_n / 1e3) / 1e9 if aug_n else 0.0
     achieved = max_over_ranks(-achieved) * -1 if dist is not None else achieved  # min over ranks
     peak = 6544.3
@@ -310,7 +363,8 @@ def run_ours(args):
     try:
         with open(PROFILE_SUMMARY) as f:
             prof = json.load(f)
-        if prof.get("dtype") == args.dtype and prof.get("per_gpu_batch") == args.per_gpu_batch:
+        if (prof.get("dtype") == args.dtype and prof.get("per_gpu_batch") == args.per_gpu_batch
+                and prof.get("kernel") == aug_kernel):
             traffic = prof["dram_bytes_per_launch"]
     except Exception:
         pass
@@ -365,7 +419,7 @@ def run_ours(args):
                 "clocks": clk.summary(),
                 "e2e": e2e,
                 "gpu_launches": int(launches1.value - launches0.value),
-                "roofline": {"bound": "hbm", "kernel": "augment_crop", "achieved": achieved,
+                "roofline": {"bound": "hbm", "kernel": aug_kernel, "achieved": achieved,
                              "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic, "peak_source": peak_src,
                              "algorithmic_bytes_per_launch": per_launch_bytes,
@@ -373,11 +427,7 @@ def run_ours(args):
                              "launches_timed": aug_n},
                 "kernel_ms": {k: (v[1] / v[0] if v[0] else None) for k, v in stats.items()},
                 "cpu_baseline": cpu,
-                "remote_per_epoch": {"loc_moved_samples": totals["moved"],
-                                     "loc_nvlink_bytes": totals["moved_nvlink"] * H * W * 3,
-                                     "reg_remote_samples": totals["reg_remote"],
-                                     "reg_remote_bytes": totals["reg_remote"] * H * W * 3,
-                                     "eq7_samples": d * (n - 1) / n}}
+                "remote_per_epoch": remote_summary(args, n, d, B, totals)}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

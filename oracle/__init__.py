@@ -105,6 +105,9 @@ def lib() -> C.CDLL:
         L.lo_cpu_crop_step.argtypes = [u8p, C.c_uint64, u64p, C.c_uint64, C.c_uint32,
                                        C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint32,
                                        C.c_uint32, f32p, f32p, C.c_int, C.c_void_p, C.c_int]
+        L.lo_cpu_resize_step.argtypes = [C.POINTER(u8p), u32p, u32p, C.c_uint64, u64p,
+                                         C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                                         C.c_uint32, f32p, f32p, C.c_int, C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -290,6 +293,32 @@ def cpu_crop_step(pool: np.ndarray, ids: np.ndarray, H: int, W: int, seed: int, 
     lib().lo_cpu_crop_step(_p(pool, C.c_uint8), pool.shape[0], _p(i, C.c_uint64), len(i), H, W,
                            seed, epoch, out_h, out_w, _p(m255, C.c_float), _p(inv, C.c_float),
                            int(bf16), out.ctypes.data_as(C.c_void_p), threads)
+
+
+class VarPool:
+    """Warm host cache of `n` variable-size samples (ids 0..n-1, true geometry)."""
+
+    def __init__(self, data_seed: int, n: int):
+        self.n = n
+        self.H = np.empty(n, np.uint32)
+        self.W = np.empty(n, np.uint32)
+        self.samples = []
+        for i in range(n):
+            h, w = sample_hw(data_seed, i)
+            self.H[i], self.W[i] = h, w
+            self.samples.append(gen_sample(data_seed, i, h * w * 3))
+        self.ptrs = (u8p * n)(*[a.ctypes.data_as(u8p) for a in self.samples])
+
+
+def cpu_resize_step(pool: VarPool, ids, seed: int, epoch: int, out: np.ndarray, bf16: bool,
+                    threads: int, out_h=224, out_w=224, mean=IMAGENET_MEAN,
+                    std=IMAGENET_STD) -> None:
+    m255, inv = norm_constants(mean, std)
+    i = np.ascontiguousarray(ids, dtype=np.uint64)
+    lib().lo_cpu_resize_step(pool.ptrs, _p(pool.H, C.c_uint32), _p(pool.W, C.c_uint32), pool.n,
+                             _p(i, C.c_uint64), len(i), seed, epoch, out_h, out_w,
+                             _p(m255, C.c_float), _p(inv, C.c_float), int(bf16),
+                             out.ctypes.data_as(C.c_void_p), threads)
 
 
 # ------------------------------------------------------------- reference (C++)

@@ -306,9 +306,23 @@ void lo_augment_one(const uint8_t* src, uint32_t H, uint32_t W, const lo_aug_par
         }
         return;
     }
-    /* RESIZE: bilinear, half-pixel centres, edge clamp. */
+    /* RESIZE: bilinear, half-pixel centres, edge clamp.  Column taps are
+     * tabulated once per sample (same arithmetic, evaluated once). */
     const float sy = (float)prm->ch / (float)out_h;
     const float sx = (float)prm->cw / (float)out_w;
+    uint32_t* txa = (uint32_t*)malloc(sizeof(uint32_t) * out_w * 2);
+    float* twx = (float*)malloc(sizeof(float) * out_w);
+    for (uint32_t ox = 0; ox < out_w; ++ox) {
+        const uint32_t mx = prm->flip ? out_w - 1 - ox : ox;
+        float fx = ((float)mx + 0.5f) * sx - 0.5f;
+        if (fx < 0.f) fx = 0.f;
+        uint32_t xlo = (uint32_t)fx;
+        if (xlo > prm->cw - 1) xlo = prm->cw - 1;
+        const uint32_t xhi = xlo + 1 < prm->cw ? xlo + 1 : prm->cw - 1;
+        twx[ox] = fx - (float)xlo;
+        txa[2 * ox] = (prm->x0 + xlo) * 3;
+        txa[2 * ox + 1] = (prm->x0 + xhi) * 3;
+    }
     for (uint32_t oy = 0; oy < out_h; ++oy) {
         float fy = ((float)oy + 0.5f) * sy - 0.5f;
         if (fy < 0.f) fy = 0.f;
@@ -319,14 +333,8 @@ void lo_augment_one(const uint8_t* src, uint32_t H, uint32_t W, const lo_aug_par
         const uint8_t* r0 = src + ((uint64_t)(prm->y0 + ylo) * W) * 3;
         const uint8_t* r1 = src + ((uint64_t)(prm->y0 + yhi) * W) * 3;
         for (uint32_t ox = 0; ox < out_w; ++ox) {
-            const uint32_t mx = prm->flip ? out_w - 1 - ox : ox;
-            float fx = ((float)mx + 0.5f) * sx - 0.5f;
-            if (fx < 0.f) fx = 0.f;
-            uint32_t xlo = (uint32_t)fx;
-            if (xlo > prm->cw - 1) xlo = prm->cw - 1;
-            const uint32_t xhi = xlo + 1 < prm->cw ? xlo + 1 : prm->cw - 1;
-            const float wx = fx - (float)xlo;
-            const uint64_t a = (uint64_t)(prm->x0 + xlo) * 3, b = (uint64_t)(prm->x0 + xhi) * 3;
+            const float wx = twx[ox];
+            const uint64_t a = txa[2 * ox], b = txa[2 * ox + 1];
             for (int c = 0; c < 3; ++c) {
                 const float p00 = (float)r0[a + c], p01 = (float)r0[b + c];
                 const float p10 = (float)r1[a + c], p11 = (float)r1[b + c];
@@ -338,6 +346,8 @@ void lo_augment_one(const uint8_t* src, uint32_t H, uint32_t W, const lo_aug_par
             }
         }
     }
+    free(txa);
+    free(twx);
 }
 
 typedef struct {
@@ -461,6 +471,57 @@ void lo_cpu_crop_step(const uint8_t* pool, uint64_t pool_n, const uint64_t* ids,
         if (t > 0) pthread_create(&tid[t], NULL, crop_worker, j);
     }
     crop_worker(&jobs[0]);
+    for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
+    free(tid);
+    free(jobs);
+}
+
+typedef struct {
+    const uint8_t* const* srcs;
+    const uint32_t* Hs;
+    const uint32_t* Ws;
+    uint64_t pool_n;
+    const uint64_t* ids;
+    uint64_t begin, end, seed, epoch;
+    uint32_t out_h, out_w;
+    const float* mean255;
+    const float* inv_std255;
+    int out_bf16;
+    void* out;
+} resize_job;
+
+static void* resize_worker(void* arg) {
+    const resize_job* j = (const resize_job*)arg;
+    const uint64_t per = 3ull * j->out_h * j->out_w * (j->out_bf16 ? 2 : 4);
+    for (uint64_t i = j->begin; i < j->end; ++i) {
+        const uint64_t slot = j->ids[i] % j->pool_n;
+        lo_aug_params prm;
+        lo_aug_params_for(j->seed, j->epoch, j->ids[i], j->Hs[slot], j->Ws[slot], j->out_h,
+                          j->out_w, LO_AUG_RESIZE, &prm);
+        lo_augment_one(j->srcs[slot], j->Hs[slot], j->Ws[slot], &prm, j->out_h, j->out_w,
+                       LO_AUG_RESIZE, j->mean255, j->inv_std255, j->out_bf16,
+                       (uint8_t*)j->out + i * per);
+    }
+    return NULL;
+}
+
+void lo_cpu_resize_step(const uint8_t* const* srcs, const uint32_t* Hs, const uint32_t* Ws,
+                        uint64_t pool_n, const uint64_t* ids, uint64_t n, uint64_t seed,
+                        uint64_t epoch, uint32_t out_h, uint32_t out_w, const float mean255[3],
+                        const float inv_std255[3], int out_bf16, void* out, int threads) {
+    if (threads < 1) threads = 1;
+    if ((uint64_t)threads > n) threads = n ? (int)n : 1;
+    pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+    resize_job* jobs = (resize_job*)malloc(sizeof(resize_job) * threads);
+    for (int t = 0; t < threads; ++t) {
+        resize_job* j = &jobs[t];
+        j->srcs = srcs; j->Hs = Hs; j->Ws = Ws; j->pool_n = pool_n; j->ids = ids;
+        j->begin = n * t / threads; j->end = n * (t + 1) / threads;
+        j->seed = seed; j->epoch = epoch; j->out_h = out_h; j->out_w = out_w;
+        j->mean255 = mean255; j->inv_std255 = inv_std255; j->out_bf16 = out_bf16; j->out = out;
+        if (t > 0) pthread_create(&tid[t], NULL, resize_worker, j);
+    }
+    resize_worker(&jobs[0]);
     for (int t = 1; t < threads; ++t) pthread_join(tid[t], NULL);
     free(tid);
     free(jobs);

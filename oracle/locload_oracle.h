@@ -139,6 +139,14 @@ void lo_cpu_crop_step(const uint8_t* pool, uint64_t pool_n, const uint64_t* ids,
                       uint32_t out_w, const float mean255[3], const float inv_std255[3],
                       int out_bf16, void* out, int threads);
 
+/* CPU-baseline driver for the variable-size workload (cfg5): sample ids[i]
+ * reads pool slot ids[i] % pool_n (srcs[slot], Hs[slot] x Ws[slot]); RESIZE
+ * parameters and lo_augment_one per sample, on `threads` threads. */
+void lo_cpu_resize_step(const uint8_t* const* srcs, const uint32_t* Hs, const uint32_t* Ws,
+                        uint64_t pool_n, const uint64_t* ids, uint64_t n, uint64_t seed,
+                        uint64_t epoch, uint32_t out_h, uint32_t out_w, const float mean255[3],
+                        const float inv_std255[3], int out_bf16, void* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif
