@@ -372,32 +372,41 @@ def run_ours(args):
     # ---- e2e: reference-facing host call, host buffers, copies in the region ----
     e2e = None
     if not args.no_e2e:
-        pinned_batch = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
         pinned_ids = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
         k_e2e = min(args.steps, 2 * spe)
+        depth = cfg.prefetch_depth
         h2d = d2h = 0
         barrier()
         t0 = time.perf_counter()
         e_cur = None
         order = None
+        outstanding = 0
         for t in range(start, start + k_e2e):
             e, s = divmod(t, spe)
             if e != e_cur:
                 order = ll.permute_epoch(SEED, e, d, device=local).order  # device plan, D2H
                 d2h += 8 * d
                 e_cur = e
-            pinned_batch[:] = order[s * B:(s + 1) * B]
-            info = ld.step_host(e, s, pinned_batch, pinned_ids)
-            h2d += 8 * B
-            d2h += 8 * info.n_local
+            ld.submit_host(e, s, order[s * B:(s + 1) * B])  # GlobalBatch from host memory
+            outstanding += 1
+            if outstanding == depth:                         # in-order delivery
+                info = ld.wait_host(pinned_ids)
+                outstanding -= 1
+                h2d += info.h2d_bytes                        # counted by the library
+                d2h += info.d2h_bytes
+        while outstanding:
+            info = ld.wait_host(pinned_ids)
+            outstanding -= 1
+            h2d += info.h2d_bytes
+            d2h += info.d2h_bytes
         barrier()
         wall = max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": sum_over_ranks(k_e2e * args.per_gpu_batch) / wall, "unit": "samples/s",
                "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e,
                "steps": k_e2e,
-               "path": "ll_loader_step_host (GlobalBatch ids from pinned host -> device "
-                       "assign/exchange/augment -> local ids to host) + ll_permute_epoch "
-                       "D2H per epoch"}
+               "path": "ll_loader_submit_host/wait_host, prefetch_depth 2: GlobalBatch ids "
+                       "from host memory -> device assign/exchange/augment -> local ids + "
+                       "step tables to host; ll_permute_epoch order D2H per epoch"}
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None

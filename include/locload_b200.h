@@ -190,6 +190,8 @@ typedef struct ll_step_info {
     uint64_t reg_remote;      /* remote samples the regular scheme would need   */
     uintptr_t device_out;     /* this step's [n_local][3][out_h][out_w] tensor  */
     uintptr_t device_ids;     /* [n_local] u32 sample ids, final list order     */
+    uint64_t h2d_bytes;       /* host->device bytes this call copied (host step) */
+    uint64_t d2h_bytes;       /* device->host bytes this call copied (host step) */
 } ll_step_info;
 
 int ll_loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg);
@@ -224,6 +226,15 @@ int ll_loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* i
 int ll_loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step,
                         const uint64_t* host_batch, uint64_t* host_local_ids,
                         ll_step_info* info);
+/* The same, pipelined like the reference's prefetching Loader (pipeline.hpp:
+ * 46-53 prefetch_depth, pipeline.cpp:283-318 in-order delivery): submit
+ * returns once the step is queued (the batch ids are copied out of
+ * host_batch), at most prefetch_depth steps may be outstanding, and wait
+ * delivers the oldest one (its local ids and info), in submission order.
+ * The step's device_out stays valid until prefetch_depth later steps. */
+int ll_loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step,
+                          const uint64_t* host_batch);
+int ll_loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* info);
 /* host copies of the current epoch plan for step `step` (tests) */
 int ll_loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
                         uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);

@@ -48,7 +48,8 @@ class StepInfo(C.Structure):
                 ("kept", C.c_uint64), ("received", C.c_uint64), ("moved_total", C.c_uint64),
                 ("nvlink_bytes", C.c_uint64), ("uncached", C.c_uint64),
                 ("reg_remote", C.c_uint64), ("device_out", C.c_size_t),
-                ("device_ids", C.c_size_t)]
+                ("device_ids", C.c_size_t), ("h2d_bytes", C.c_uint64),
+                ("d2h_bytes", C.c_uint64)]
 
 
 class Xfer(C.Structure):
@@ -113,6 +114,8 @@ PROTOTYPES = {
     "ll_loader_step": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.POINTER(StepInfo)]),
     "ll_loader_step_host": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p, u64p,
                                       C.POINTER(StepInfo)]),
+    "ll_loader_submit_host": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, u64p]),
+    "ll_loader_wait_host": (C.c_int, [C.c_void_p, u64p, C.POINTER(StepInfo)]),
     "ll_loader_plan_step": (C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, u64p, u64p,
                                       C.POINTER(Move), u32p]),
     "ll_loader_epoch_totals": (C.c_int, [C.c_void_p, u64p]),

@@ -29,6 +29,8 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch);
 void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* info);
 void loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch,
                       uint64_t* host_local_ids, ll_step_info* info);
+void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch);
+void loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* info);
 void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
                       uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);
 void loader_epoch_totals(ll_loader* ld, uint64_t* out4);
@@ -484,6 +486,13 @@ int ll_loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step,
                         const uint64_t* host_batch, uint64_t* host_local_ids,
                         ll_step_info* info) {
     return guarded([&] { loader_step_host(ld, epoch, step, host_batch, host_local_ids, info); });
+}
+int ll_loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step,
+                          const uint64_t* host_batch) {
+    return guarded([&] { loader_submit_host(ld, epoch, step, host_batch); });
+}
+int ll_loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* info) {
+    return guarded([&] { loader_wait_host(ld, host_local_ids, info); });
 }
 int ll_loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
                         uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves) {

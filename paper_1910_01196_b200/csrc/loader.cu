@@ -54,10 +54,6 @@ struct ll_loader {
     int64_t plan_epoch = -1;
     std::vector<ll_move> h_moves;
     std::vector<uint32_t> h_off, h_kept, h_counts, h_nmoves, h_stats;
-    // single-step plan for the host-driven entry point
-    ll::DevBuf e2e_batch64, e2e_order;
-    ll::PlanBufs e2e_plan;
-    ll::DevBuf e2e_ids64;
     // exchange
     ncclComm_t comm = nullptr;
     ll::DevBuf packbuf, recvbuf;
@@ -67,6 +63,29 @@ struct ll_loader {
     // output ring
     std::vector<std::unique_ptr<ll::DevBuf>> out;
     uint32_t out_slot = 0;
+    // host-driven steps in flight (ll_loader_submit_host / wait_host), at most
+    // prefetch_depth outstanding, delivered in submission order
+    struct Tables {  // one step's plan tables as delivered to the host
+        ll_move moves[ll::kMaxP];
+        uint32_t off[ll::kMaxP + 1], kept[ll::kMaxP], n, stats[4];
+    };
+    struct HostSlot {
+        uint64_t* pin = nullptr;         // pinned: [Tables][B x u64 local ids]
+        uint64_t* pin_batch = nullptr;   // pinned copy of the caller's GlobalBatch
+        ll::DevBuf batch64, order, stage;  // device: batch, narrowed batch, staging
+        ll::PlanBufs plan;               // this step's single-step plan
+        cudaEvent_t pro_done = nullptr;  // prologue (H2D + assign) finished (side stream)
+        cudaEvent_t done = nullptr;      // whole step finished (main stream)
+        bool used = false;
+        ll_step_info info{};
+        uint64_t n_local = 0;
+        bool synchronous = false;
+        Tables* tab() const { return reinterpret_cast<Tables*>(pin); }
+        uint64_t* ids() const { return pin + sizeof(Tables) / 8; }
+    };
+    std::vector<std::unique_ptr<HostSlot>> hslots;
+    uint64_t submitted = 0, waited = 0;
+    cudaStream_t side = nullptr;     // prologue stream of host-driven steps
 };
 
 namespace ll {
@@ -214,6 +233,69 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     }
 }
 
+// A step whose plan tables stay on the device (host-driven path): the list
+// offset and kept count are read by the kernel, n_local is the balanced
+// target (or the regular slice), so no mid-step host sync is needed.
+void* run_step_devplan(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t n_local) {
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const uint32_t me = c.rank, p = c.learners;
+    SrcMap src;
+    src.kind = 1;
+    src.list = pd.final_ids;
+    src.list_off = pd.off + me;
+    src.kept_dev = pd.kept + me;
+    src.shard = ld->shard.as<uint8_t>();
+    src.shard_first = ld->first;
+    src.p = p;
+    src.cached = ld->cached;
+    src.sample_bytes = ld->S;
+    if (c.geometry == LL_GEOM_VARIABLE) {
+        src.prefix = ld->prefix.as<uint64_t>();
+        src.data_seed = c.data_seed;
+    }
+    if (c.augment.mode == LL_AUG_CROP) src.aug = pd.aug;
+    if (p > 1) {
+        require(ld->peers_ready, "loader: P2P exchange needs peer shards (open/link)");
+        src.peers = ld->d_peers.as<const uint8_t*>();
+        if (c.scheme == LL_SCHEME_REGULAR) {
+            src.kept_dev = nullptr;
+            src.kept = 0;
+        }
+    }
+    ensure_out(ld);
+    void* out = ld->out[ld->out_slot]->ptr;
+    ld->out_slot = (ld->out_slot + 1) % ld->out.size();
+    const uint32_t gh = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.height;
+    const uint32_t gw = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.width;
+    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, gh, gw, out);
+    return out;
+}
+
+// Stage one host-driven step's results for a single D2H copy:
+// [Tables][n_local x u64 ids].
+__global__ void k_stage(PlanDev pd, uint32_t me, uint32_t p, uint8_t* __restrict__ stage,
+                        uint64_t n) {
+    auto* t = reinterpret_cast<ll_loader::Tables*>(stage);
+    uint64_t* ids = reinterpret_cast<uint64_t*>(stage + sizeof(ll_loader::Tables));
+    const uint32_t base = pd.off[me];
+    const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    for (uint64_t i = tid; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        ids[i] = pd.final_ids[base + i];
+    if (blockIdx.x == 0) {
+        const uint32_t nm = *pd.n_moves;
+        for (uint32_t j = threadIdx.x; j < kMaxP; j += blockDim.x) {
+            if (j < nm) t->moves[j] = pd.moves[j];
+            if (j < p) {
+                t->kept[j] = pd.kept[j];
+            }
+        }
+        for (uint32_t j = threadIdx.x; j <= p; j += blockDim.x) t->off[j] = pd.off[j];
+        if (threadIdx.x < 4) t->stats[threadIdx.x] = pd.stats[threadIdx.x];
+        if (threadIdx.x == 0) t->n = nm;
+    }
+}
+
 } // namespace
 
 void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
@@ -280,6 +362,14 @@ void loader_destroy(ll_loader* ld) {
     if (!ld) return;
     cudaSetDevice(ld->ctx->device);
     for (void* p : ld->peer_open) cudaIpcCloseMemHandle(p);
+    for (auto& hp : ld->hslots) {
+        auto& h = *hp;
+        if (h.pin) cudaFreeHost(h.pin);
+        if (h.pin_batch) cudaFreeHost(h.pin_batch);
+        if (h.pro_done) cudaEventDestroy(h.pro_done);
+        if (h.done) cudaEventDestroy(h.done);
+    }
+    if (ld->side) cudaStreamDestroy(ld->side);
     if (ld->comm) ncclCommDestroy(ld->comm);
     delete ld;
 }
@@ -392,46 +482,142 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
              &ld->h_stats[step * 4], info);
 }
 
-void loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch,
-                      uint64_t* host_local_ids, ll_step_info* info) {
+void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch) {
     require(ld->populated, "Loader: shard not populated");
     set_device(ld->ctx);
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     const uint64_t B = c.batch_size;
-    ld->e2e_batch64.reserve(sizeof(uint64_t) * B);
-    ld->e2e_order.reserve(sizeof(uint32_t) * B);
-    ld->e2e_plan.reserve(1, B);
-    LL_CUDA(cudaMemcpyAsync(ld->e2e_batch64.ptr, host_batch, sizeof(uint64_t) * B,
-                            cudaMemcpyHostToDevice, ctx->stream));
-    narrow_device(ctx, ld->e2e_batch64.as<uint64_t>(), ld->e2e_order.as<uint32_t>(), B);
-    assign_device(ctx, ld->e2e_order.as<uint32_t>(), 1, B, c.learners, ld->cached, c.scheme,
-                  ld->e2e_plan.view(), aug_plan(ld, epoch));
-    // the host needs this step's counts to size the grid and the messages
-    ll_move h_moves[kMaxP];
-    uint32_t h_off[kMaxP + 1], h_kept[kMaxP], h_n = 0, h_stats[4];
-    LL_CUDA(cudaMemcpyAsync(h_moves, ld->e2e_plan.moves.ptr, sizeof(h_moves),
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    LL_CUDA(cudaMemcpyAsync(h_off, ld->e2e_plan.off.ptr, sizeof(h_off), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    LL_CUDA(cudaMemcpyAsync(h_kept, ld->e2e_plan.kept.ptr, sizeof(h_kept),
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    LL_CUDA(cudaMemcpyAsync(&h_n, ld->e2e_plan.n_moves.ptr, sizeof(h_n), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    LL_CUDA(cudaMemcpyAsync(h_stats, ld->e2e_plan.stats.ptr, sizeof(h_stats),
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    LL_CUDA(cudaStreamSynchronize(ctx->stream));
-    ll_step_info local{};
-    run_step(ld, epoch, ld->e2e_plan.view(), 0, h_moves, h_off, h_kept, h_n, h_stats, &local);
-    local.step = step;
-    const uint64_t n_local = local.n_local;
-    ld->e2e_ids64.reserve(sizeof(uint64_t) * std::max<uint64_t>(n_local, 1));
-    widen_device(ctx, ld->e2e_plan.final_ids.as<uint32_t>() + h_off[c.rank],
-                 ld->e2e_ids64.as<uint64_t>(), n_local);
-    LL_CUDA(cudaMemcpyAsync(host_local_ids, ld->e2e_ids64.ptr, sizeof(uint64_t) * n_local,
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    LL_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (info) *info = local;
+    const uint32_t p = c.learners, me = c.rank;
+    const uint32_t F = std::max<uint32_t>(1, c.prefetch_depth);
+    require(ld->submitted - ld->waited < F,
+            "Loader: prefetch_depth host steps already outstanding (wait first)");
+    if (ld->hslots.empty()) {
+        for (uint32_t f = 0; f < F; ++f) ld->hslots.emplace_back(new ll_loader::HostSlot());
+        for (auto& hp : ld->hslots) {
+            auto& h = *hp;
+            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h.pin),
+                                  sizeof(ll_loader::Tables) + sizeof(uint64_t) * B, 0));
+            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h.pin_batch), sizeof(uint64_t) * B, 0));
+            LL_CUDA(cudaEventCreateWithFlags(&h.pro_done, cudaEventDisableTiming));
+            LL_CUDA(cudaEventCreateWithFlags(&h.done, cudaEventDisableTiming));
+            h.batch64.reserve(sizeof(uint64_t) * B);
+            h.order.reserve(sizeof(uint32_t) * B);
+            h.stage.reserve(sizeof(ll_loader::Tables) + sizeof(uint64_t) * B);
+            h.plan.reserve(1, B);
+        }
+        LL_CUDA(cudaStreamCreateWithFlags(&ld->side, cudaStreamNonBlocking));
+    }
+    auto& h = *ld->hslots[ld->submitted % F];
+    h.info = ll_step_info{};
+    h.info.epoch = epoch;
+    h.info.step = step;
+    std::memcpy(h.pin_batch, host_batch, sizeof(uint64_t) * B);
+    // prologue (H2D + assignment) on the side stream, so it overlaps the
+    // previous step's augment; it may reuse this slot only after the step that
+    // last used it has finished on the main stream
+    cudaStream_t main = ctx->stream;
+    if (h.used) LL_CUDA(cudaStreamWaitEvent(ld->side, h.done, 0));
+    ctx->stream = ld->side;
+    try {
+        LL_CUDA(cudaMemcpyAsync(h.batch64.ptr, h.pin_batch, sizeof(uint64_t) * B,
+                                cudaMemcpyHostToDevice, ctx->stream));
+        narrow_device(ctx, h.batch64.as<uint64_t>(), h.order.as<uint32_t>(), B);
+        assign_device(ctx, h.order.as<uint32_t>(), 1, B, p, ld->cached, c.scheme, h.plan.view(),
+                      aug_plan(ld, epoch));
+        LL_CUDA(cudaEventRecord(h.pro_done, ctx->stream));
+    } catch (...) {
+        ctx->stream = main;
+        throw;
+    }
+    ctx->stream = main;
+    LL_CUDA(cudaStreamWaitEvent(main, h.pro_done, 0));
+    h.used = true;
+    h.info.h2d_bytes = sizeof(uint64_t) * B;
+    const PlanDev pd = h.plan.view();
+    const bool devplan = (c.scheme == LL_SCHEME_LOCALITY_BALANCED ||
+                          c.scheme == LL_SCHEME_REGULAR) &&
+                         (p == 1 || c.exchange == LL_EXCHANGE_P2P);
+    h.synchronous = !devplan;
+    const size_t tab = sizeof(ll_loader::Tables);
+    if (devplan) {
+        // fully asynchronous: the kernel reads the list offset and kept count
+        // from the device plan; n_local is the balanced target / regular slice
+        h.n_local = B / p + (me < B % p ? 1 : 0);
+        void* out = run_step_devplan(ld, epoch, pd, h.n_local);
+        launch(ctx, "stage", [&] {
+            k_stage<<<static_cast<unsigned>(std::min<uint64_t>((h.n_local + 255) / 256 + 1, 1184)),
+                      256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), h.n_local);
+        });
+        LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab + sizeof(uint64_t) * h.n_local,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        h.info.d2h_bytes = tab + sizeof(uint64_t) * h.n_local;
+        h.info.device_out = reinterpret_cast<uintptr_t>(out);
+    } else {
+        // NCCL exchange / unbalanced lists: the host needs the counts to size
+        // the grid and the messages before issuing the rest of the step
+        launch(ctx, "stage", [&] {
+            k_stage<<<1, 256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), 0);
+        });
+        LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab, cudaMemcpyDeviceToHost, ctx->stream));
+        LL_CUDA(cudaStreamSynchronize(ctx->stream));
+        const auto* t = h.tab();
+        ll_step_info local{};
+        run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local);
+        local.h2d_bytes = h.info.h2d_bytes;
+        local.d2h_bytes = tab;
+        h.info = local;
+        h.n_local = local.n_local;
+        launch(ctx, "stage", [&] {
+            k_stage<<<static_cast<unsigned>(std::min<uint64_t>((h.n_local + 255) / 256 + 1, 1184)),
+                      256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), h.n_local);
+        });
+        LL_CUDA(cudaMemcpyAsync(h.ids(), h.stage.as<uint8_t>() + tab,
+                                sizeof(uint64_t) * h.n_local, cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        h.info.d2h_bytes += sizeof(uint64_t) * h.n_local;
+    }
+    h.info.step = step;
+    h.info.epoch = epoch;
+    LL_CUDA(cudaEventRecord(h.done, ctx->stream));
+    ++ld->submitted;
+}
+
+void loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* info) {
+    require(ld->waited < ld->submitted, "Loader: no host step outstanding");
+    set_device(ld->ctx);
+    const uint32_t F = std::max<uint32_t>(1, ld->cfg.prefetch_depth);
+    auto& h = *ld->hslots[ld->waited % F];
+    LL_CUDA(cudaEventSynchronize(h.done));
+    const uint32_t me = ld->cfg.rank, p = ld->cfg.learners;
+    if (!h.synchronous) {
+        const auto* t = h.tab();
+        uint64_t recv = 0, nvl = 0;
+        for (uint32_t m = 0; m < t->n; ++m)
+            if (t->moves[m].receiver == me) {
+                recv += t->moves[m].count;
+                nvl += t->moves[m].nvlink;
+            }
+        const bool reg = p > 1 && ld->cfg.scheme == LL_SCHEME_REGULAR;
+        h.info.n_local = h.n_local;
+        h.info.kept = reg ? 0 : t->kept[me];
+        h.info.received = reg ? h.n_local : recv;
+        h.info.moved_total = t->stats[0];
+        h.info.nvlink_bytes = nvl * ld->S;
+        h.info.uncached = t->stats[2];
+        h.info.reg_remote = t->stats[3] == 0xFFFFFFFFu ? UINT64_MAX : t->stats[3];
+        h.info.device_ids = reinterpret_cast<uintptr_t>(h.plan.final_ids.as<uint32_t>() + t->off[me]);
+    }
+    if (host_local_ids) std::memcpy(host_local_ids, h.ids(), sizeof(uint64_t) * h.n_local);
+    if (info) *info = h.info;
+    ++ld->waited;
+}
+
+void loader_step_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch,
+                      uint64_t* host_local_ids, ll_step_info* info) {
+    require(ld->waited == ld->submitted, "Loader: host steps still outstanding");
+    loader_submit_host(ld, epoch, step, host_batch);
+    loader_wait_host(ld, host_local_ids, info);
 }
 
 void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,

@@ -170,6 +170,17 @@ class DeviceLoader:
                                               ptr(out_ids, C.c_uint64), C.byref(info)))
         return info
 
+    def submit_host(self, epoch: int, step: int, batch: np.ndarray) -> None:
+        """Queue one host-driven step (at most prefetch_depth outstanding)."""
+        b = np.ascontiguousarray(batch, dtype=np.uint64)
+        check(_capi.lib().ll_loader_submit_host(self._h, epoch, step, ptr(b, C.c_uint64)))
+
+    def wait_host(self, out_ids: np.ndarray):
+        """Deliver the oldest outstanding host step: (info) with out_ids filled."""
+        info = _capi.StepInfo()
+        check(_capi.lib().ll_loader_wait_host(self._h, ptr(out_ids, C.c_uint64), C.byref(info)))
+        return info
+
     def plan_step(self, step: int):
         B, p = self.cfg.batch_size, self.cfg.learners
         ids = np.empty(B, np.uint64)

@@ -485,3 +485,29 @@ def test_loader_variable_size_resize_vs_oracle(dtype):
                 else:
                     assert bf16_ulps(got[k], want) <= 1
                 assert np.array_equal(got[k], want), (t, j, k, H, W)
+
+
+def test_loader_host_submit_wait_pipelined():
+    """Prefetching host API (prefetch_depth 2): in-order delivery, identical
+    to the synchronous call and to the device-planned step."""
+    d, p, B = 8192, 2, 512
+    lds = make_learners(d, p, B)
+    order = ll.permute_epoch(42, 4, d).order
+    ld = lds[0]
+    want = []
+    for t in range(5):
+        want.append(ld.fetch_ids(ld.step(4, t)).copy())
+    ld.submit_host(4, 0, order[0:B])
+    ld.submit_host(4, 1, order[B:2 * B])
+    with pytest.raises(ValueError, match="outstanding"):
+        ld.submit_host(4, 2, order[2 * B:3 * B])
+    ids = np.empty(B, np.uint64)
+    for t in range(5):
+        info = ld.wait_host(ids)
+        assert info.step == t
+        assert np.array_equal(ids[:info.n_local], want[t])
+        assert info.h2d_bytes == 8 * B and info.d2h_bytes >= 8 * info.n_local
+        if t + 2 < 5:
+            ld.submit_host(4, t + 2, order[(t + 2) * B:(t + 3) * B])
+    with pytest.raises(ValueError, match="no host step"):
+        ld.wait_host(ids)
