@@ -49,8 +49,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=1560)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg5"],
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg2: fixed 256x256 crop224 (default, the headline); "
+                         "cfg3: cfg2 with each learner caching 25%% of the dataset "
+                         "(alpha = min(1, 0.25 N); uncached samples from the pinned host "
+                         "storage tier); cfg4: cfg2 under the regular (naive "
+                         "DistributedSampler) scheme, remote samples read over NVLink; "
                          "cfg5: variable 128-512 px, bilinear resize to 224")
     ap.add_argument("--dtype", default=None, choices=["fp32", "bf16"],
                     help="output dtype (default fp32 for cfg2, bf16 for cfg5)")
@@ -78,8 +82,22 @@ def src_bytes_per_sample(args) -> float:
     return mean_window_bytes_cfg5() if args.workload == "cfg5" else float(SRC_BYTES)
 
 
+
+def alpha_for(args, n) -> float:
+    return min(1.0, 0.25 * n) if args.workload == "cfg3" else 1.0
+
+
 def workload(args, n):
-    if args.workload == "cfg5":
+    if args.workload in ("cfg3", "cfg4"):
+        a = alpha_for(args, n)
+        name = ("cfg3-weak: cfg2 shapes, 25% of the dataset cached per learner "
+                f"(alpha={a:g}; uncached samples read from the pinned host storage tier)"
+                if args.workload == "cfg3" else
+                "cfg4-weak: cfg2 shapes under the regular scheme (reg_slice; every "
+                "non-owned sample read from its owner's HBM over NVLink)")
+        name += (f", d={args.per_gpu_d}*N, p=N, global batch {args.per_gpu_batch}*N, "
+                 f"crop224+flip+normalize -> NCHW {args.dtype}")
+    elif args.workload == "cfg5":
         name = ("cfg5-weak: variable-size synthetic u8 HWC (H, W uniform 128-512 px), "
                 f"d={args.per_gpu_d}*N, p=N, global batch {args.per_gpu_batch}*N, alpha=1, "
                 f"locality_balanced, random square crop + flip + bilinear resize 224 + "
@@ -90,7 +108,8 @@ def workload(args, n):
                 f"alpha=1, locality_balanced, crop224+flip+normalize -> NCHW {args.dtype}")
     return {"workload": name,
             "d": args.per_gpu_d * n, "learners": n, "global_batch": args.per_gpu_batch * n,
-            "per_gpu_batch": args.per_gpu_batch, "alpha": 1.0, "scheme": "locality_balanced",
+            "per_gpu_batch": args.per_gpu_batch, "alpha": alpha_for(args, n),
+            "scheme": "regular" if args.workload == "cfg4" else "locality_balanced",
             "exchange": args.exchange if n > 1 else "none", "out_dtype": args.dtype,
             "l2": "inputs larger than L2 (31.5 GB shard, 616 MB output/step); no flush",
             "timed_region": "starts at an epoch boundary; epoch plans included"}
@@ -207,7 +226,7 @@ def remote_summary(args, n, d, B, totals):
     device plan) vs the regular scheme's remote samples (counted in the same
     plan) vs the paper's model, Eq. 7 (alpha*D*(p-1)/p) and Eq. 8
     (alpha*D*beta) with beta measured as moved/B (model.hpp:65-74)."""
-    per = H * W * 3 if args.workload == "cfg2" else mean_window_bytes_cfg5() / 1.0
+    per = mean_window_bytes_cfg5() if args.workload == "cfg5" else H * W * 3
     steps = d // B
     beta = totals["moved"] / (steps * B) if steps else 0.0
     return {"loc_moved_samples": totals["moved"],
@@ -217,7 +236,9 @@ def remote_summary(args, n, d, B, totals):
             "bytes_per_sample": per,
             "loc_remote_bytes": totals["moved_nvlink"] * per,
             "reg_remote_bytes": totals["reg_remote"] * per,
-            "local_fraction": 1.0 - (totals["moved"] / (steps * B) if steps else 0.0)}
+            "local_fraction": 1.0 - (totals["moved"] / (steps * B) if steps else 0.0),
+            "storage_samples": totals["uncached"],
+            "storage_window_bytes": totals["uncached"] * src_bytes_per_sample(args)}
 
 
 def run_reference(args):
@@ -260,8 +281,9 @@ def run_ours(args):
 
     d, B = args.per_gpu_d * n, args.per_gpu_batch * n
     cfg5 = args.workload == "cfg5"
-    cfg = LoaderConfig(d=d, height=H, width=W, learners=n, rank=rank, batch_size=B, alpha=1.0,
-                       seed=SEED, data_seed=SEED, scheme="locality_balanced",
+    cfg = LoaderConfig(d=d, height=H, width=W, learners=n, rank=rank, batch_size=B,
+                       alpha=alpha_for(args, n), seed=SEED, data_seed=SEED,
+                       scheme="regular" if args.workload == "cfg4" else "locality_balanced",
                        exchange=args.exchange if n > 1 else "none", prefetch_depth=2,
                        geometry="variable" if cfg5 else "fixed",
                        augment=AugmentConfig(mode="resize" if cfg5 else "crop",

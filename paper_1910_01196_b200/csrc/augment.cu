@@ -70,7 +70,10 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
     const uint32_t kept = m.kept_dev ? *m.kept_dev : m.kept;
     const uint64_t s = list[k];
     *id = s;
-    if (k < kept) {
+    if (s >= m.cached && m.storage) {
+        // storage tier (alpha < 1): uncached samples from mapped pinned host memory
+        *src = m.storage + (s - m.cached) * m.sample_bytes;
+    } else if (k < kept) {
         *src = m.shard + (m.prefix ? m.prefix[s] - m.prefix[m.shard_first]
                                    : (s - m.shard_first) * m.sample_bytes);
     } else if (m.peers) {

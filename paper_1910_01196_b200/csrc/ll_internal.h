@@ -179,6 +179,9 @@ struct SrcMap {
     // geometry from the id (geometry.cuh); recv/explicit paths need fixed size
     const uint64_t* prefix = nullptr;
     uint64_t data_seed = 0;
+    // storage tier (alpha < 1): sample s >= cached at storage + (s - cached) * bytes,
+    // a mapped pinned host buffer read over PCIe / C2C by the kernel itself
+    const uint8_t* storage = nullptr;
 };
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
                     const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out);

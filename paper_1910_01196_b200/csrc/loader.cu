@@ -47,6 +47,7 @@ struct ll_loader {
     ll::DevBuf shard;
     bool populated = false;
     ll::DevBuf prefix;            // variable geometry: global padded-size prefix [d+1]
+    uint8_t* storage = nullptr;   // alpha < 1: pinned+mapped host copy of ids [cached, d)
     std::vector<uint64_t> h_prefix_ends;  // prefix at first and first+owned
     // epoch plan
     ll::DevBuf order;
@@ -169,6 +170,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     src.p = p;
     src.cached = ld->cached;
     src.sample_bytes = ld->S;
+    src.storage = ld->storage;
     if (c.geometry == LL_GEOM_VARIABLE) {
         src.prefix = ld->prefix.as<uint64_t>();
         src.data_seed = c.data_seed;
@@ -250,6 +252,7 @@ void* run_step_devplan(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_
     src.p = p;
     src.cached = ld->cached;
     src.sample_bytes = ld->S;
+    src.storage = ld->storage;
     if (c.geometry == LL_GEOM_VARIABLE) {
         src.prefix = ld->prefix.as<uint64_t>();
         src.data_seed = c.data_seed;
@@ -330,7 +333,12 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
     ld->cached = static_cast<uint64_t>(c.alpha * static_cast<double>(c.d));  // sampling.cpp:15
     if (ld->cached > c.d) ld->cached = c.d;
     require(ld->cached >= 1, "Loader: alpha * d must cache at least one sample");
-    require(ld->cached == c.d, "Loader: alpha < 1 needs the storage tier (not built yet)");
+    if (ld->cached < c.d) {
+        require(c.geometry == LL_GEOM_FIXED,
+                "Loader: the storage tier (alpha < 1) supports fixed-size samples");
+        require(c.learners == 1 || c.exchange == LL_EXCHANGE_P2P,
+                "Loader: the storage tier (alpha < 1) needs the P2P exchange");
+    }
     const uint64_t p = c.learners, j = c.rank;
     ld->first = (j * ld->cached + p - 1) / p;
     ld->owned = ((j + 1) * ld->cached + p - 1) / p - ld->first;
@@ -370,6 +378,7 @@ void loader_destroy(ll_loader* ld) {
         if (h.done) cudaEventDestroy(h.done);
     }
     if (ld->side) cudaStreamDestroy(ld->side);
+    if (ld->storage) cudaFreeHost(ld->storage);
     if (ld->comm) ncclCommDestroy(ld->comm);
     delete ld;
 }
@@ -431,8 +440,31 @@ void loader_link_peers(ll_loader* const* lds, uint32_t n) {
     }
 }
 
+// Storage tier for alpha < 1: every uncached sample (ids [cached, d)) in one
+// pinned, device-mapped host buffer, filled with the generate_dataset bytes in
+// device-generated chunks.  The augment kernel reads crop windows from it
+// directly (zero-copy over PCIe / NVLink-C2C) -- the "storage system" path of
+// the paper's cost model (model.hpp:65-74), counted separately from NVLink.
+void populate_storage(ll_loader* ld) {
+    const uint64_t n = ld->cfg.d - ld->cached;
+    if (n == 0 || ld->storage) return;
+    ll_ctx* ctx = ld->ctx;
+    LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ld->storage), n * ld->S,
+                          cudaHostAllocMapped | cudaHostAllocPortable));
+    const uint64_t chunk = std::max<uint64_t>(1, (1ull << 30) / ld->S);
+    DevBuf& tmp = ctx->buf("storage.stage", chunk * ld->S);
+    for (uint64_t i = 0; i < n; i += chunk) {
+        const uint64_t m = std::min(chunk, n - i);
+        generate_range_device(ctx, tmp.as<uint8_t>(), ld->cached + i, m, ld->S, ld->cfg.data_seed);
+        LL_CUDA(cudaMemcpyAsync(ld->storage + i * ld->S, tmp.ptr, m * ld->S,
+                                cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    LL_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
 void loader_populate(ll_loader* ld) {
     set_device(ld->ctx);
+    populate_storage(ld);
     if (ld->cfg.geometry == LL_GEOM_VARIABLE)
         generate_var_device(ld->ctx, ld->shard.as<uint8_t>(), ld->first, ld->owned,
                             ld->prefix.as<uint64_t>(), ld->cfg.data_seed);
@@ -445,6 +477,7 @@ void loader_populate(ll_loader* ld) {
 
 void loader_populate_from_host(ll_loader* ld, const uint8_t* host) {
     set_device(ld->ctx);
+    require(ld->cached == ld->cfg.d, "Loader: populate_from_host needs alpha = 1");
     require(ld->cfg.geometry == LL_GEOM_FIXED,
             "Loader: populate_from_host supports fixed-size samples");
     LL_CUDA(cudaMemcpyAsync(ld->shard.ptr, host, ld->owned * ld->S, cudaMemcpyHostToDevice,

@@ -1,13 +1,24 @@
 #!/bin/bash
-# multi-GPU: exchange tests + bench at N=2 (p2p and nccl)
+# multi-GPU: exchange tests + bench lines at N GPUs for every workload
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 N=${N:-2}
-nvidia-smi topo -m > gpurun_out/topo.txt 2>&1
-timeout 900 python -m pytest tests/test_gpu_multi.py -q --timeout 600 -rf > gpurun_out/pytest_multi.log 2>&1
-echo "pytest multi rc=$?"; tail -5 gpurun_out/pytest_multi.log
-for X in p2p nccl; do
-timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
-   --master-port 29511 bench.py --gpus $N --steps 312 --warmup 5 --exchange $X > gpurun_out/bench_n${N}_${X}.log 2>&1
-echo "bench $X rc=$?"; tail -2 gpurun_out/bench_n${N}_${X}.log | cut -c1-600
-done
+TAG=${TAG:-r01}
+nvidia-smi topo -m > gpurun_out/topo_n${N}.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_multi.py -q --timeout 600 -rf > gpurun_out/pytest_multi_n${N}.log 2>&1
+echo "pytest multi rc=$?"; tail -2 gpurun_out/pytest_multi_n${N}.log
+run() {
+  local name=$1; shift
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
+     --master-port 29511 bench.py --gpus $N "$@" > gpurun_out/bench_${TAG}_n${N}_${name}.log 2>&1
+  echo "bench $name rc=$?"; tail -1 gpurun_out/bench_${TAG}_n${N}_${name}.log | python -c "
+import json,sys
+try:
+    l=json.loads(sys.stdin.read()); print(round(l['value']), round(l['ms_per_step'],4), 'e2e', round(l['e2e']['value']) if l.get('e2e') else None, 'roof', round(l['roofline']['frac'],3), l['remote_per_epoch'])
+except Exception as e: print('parse fail', e)"
+}
+run cfg2_p2p --steps ${STEPS:-624}
+run cfg2_nccl --steps ${STEPS:-624} --exchange nccl
+run cfg3 --workload cfg3 --steps ${STEPS:-312}
+run cfg4 --workload cfg4 --steps ${STEPS:-312}
+run cfg5 --workload cfg5 --steps ${STEPS:-312}

@@ -511,3 +511,33 @@ def test_loader_host_submit_wait_pipelined():
             ld.submit_host(4, t + 2, order[(t + 2) * B:(t + 3) * B])
     with pytest.raises(ValueError, match="no host step"):
         ld.wait_host(ids)
+
+
+@pytest.mark.parametrize("p,alpha", [(1, 0.25), (2, 0.5), (3, 0.37)])
+def test_loader_storage_tier_vs_oracle(p, alpha):
+    """alpha < 1 (cfg3): uncached samples are dealt round-robin (counts as the
+    reference, order as DESIGN.md section 3) and read from the pinned host
+    storage tier; every learner's batch equals the oracle's."""
+    d, B, seed = 3000, 120, 42
+    lds = []
+    for j in range(p):
+        ld = DeviceLoader(LoaderConfig(d=d, learners=p, rank=j, batch_size=B, alpha=alpha,
+                                       seed=seed, data_seed=seed, exchange="p2p"))
+        ld.populate()
+        lds.append(ld)
+    if p > 1:
+        DeviceLoader.link_peers(lds)
+    cached = oracle.cached_count(d, alpha)
+    order = oracle.permute_epoch(seed, 1, d)
+    for t in [0, 13]:
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, cached, oracle.MODE_LOCALITY_BALANCED)
+        for j, ld in enumerate(lds):
+            info = ld.step(1, t)
+            lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            assert info.uncached == int((order[t * B:(t + 1) * B] >= cached).sum())
+            got = ld.fetch(info)
+            src = oracle.gen_samples(seed, lst, 256 * 256 * 3)
+            for k, sid in enumerate(lst):
+                want = oracle.augment(src[k].reshape(256, 256, 3), int(sid), seed, 1)
+                assert np.array_equal(got[k], want), (t, j, k, int(sid) >= cached)
