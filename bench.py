@@ -398,6 +398,11 @@ def run_ours(args):
         k_e2e = min(args.steps, 2 * spe)
         depth = cfg.prefetch_depth
         h2d = d2h = 0
+        # warm-up of the host path (pinned slots, side stream, first launches)
+        wo = ll.permute_epoch(SEED, 0, d, device=local).order
+        for s_ in range(min(args.warmup, spe)):
+            ld.submit_host(0, s_, wo[s_ * B:(s_ + 1) * B])
+            ld.wait_host(pinned_ids)
         barrier()
         t0 = time.perf_counter()
         e_cur = None
