@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "liblocload_b200.so")
+LIB_PATH = os.environ.get("LL_LIB", os.path.join(HERE, "liblocload_b200.so"))
 
 LL_OK, LL_ERR_INVALID, LL_ERR_RUNTIME, LL_ERR_CUDA, LL_ERR_NCCL, LL_ERR_UNSUPPORTED = range(6)
 SCHEME_REGULAR, SCHEME_LOCALITY, SCHEME_LOCALITY_BALANCED = 0, 1, 2

@@ -35,7 +35,11 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), lib=None) -> str:
+    global LIB
+    if lib is not None:  # variant builds for A/B measurements
+        LIB = lib
+        force = True
     if not force and not _stale():
         return LIB
     objdir = os.path.join(HERE, "build")
@@ -44,7 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     logs = []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.basename(src).rsplit(".", 1)[0] + ".o")
-        cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:

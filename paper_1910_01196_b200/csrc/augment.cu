@@ -242,7 +242,9 @@ __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, 
 // PX output pixels per thread: 4 (fp32, one float4 per plane) or 8 (bf16,
 // eight bf16 per plane).  kThreads/(224/PX) = PX rows per pass.
 template <bool BF16, int DBG = 0>
-__global__ void __launch_bounds__(kThreads) k_augment_crop(AugArgs a) {
+// (measured: 4 resident CTAs per SM at 72 registers beat forcing 5-9 by
+// register caps or a larger shared-memory carveout; profiles/r01_augment_ab.md)
+__global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
     __shared__ const uint8_t* s_src;
     __shared__ Params s_prm;
