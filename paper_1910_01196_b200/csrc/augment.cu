@@ -161,7 +161,7 @@ __device__ __forceinline__ uint32_t bf16x2(uint64_t v) {
 // realigned with funnel shifts (the shift is uniform per sample); each byte
 // becomes a float through PRMT + exact subtraction, and the normalisation
 // runs on packed fp32x2 -- no I2F, same IEEE results as the oracle.
-template <bool BF16, bool FLIP, int DBG = 0>
+template <bool BF16, bool FLIP>
 __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint64_t const* mean2,
                                          uint64_t const* inv2, void* out, uint64_t o,
                                          uint64_t plane) {
@@ -195,7 +195,6 @@ __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint6
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        if (DBG == 2 && lo32(v[c][0]) != 0x12345u) continue;  // debug: compute, no stores
         if constexpr (BF16) {
             st_cs_v4(static_cast<uint16_t*>(out) + o + c * plane,
                      make_uint4(bf16x2(v[c][0]), bf16x2(v[c][1]), bf16x2(v[c][2]),
@@ -209,7 +208,7 @@ __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint6
 
 // Rows [r_first, r_first + kBand) of the band: thread (tr, tq) writes pixel run
 // tq of rows tr, tr + PX, ...
-template <bool BF16, int DBG = 0>
+template <bool BF16>
 __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, uint32_t a0,
                                           uint64_t k, uint32_t band, const NormConst& nc,
                                           void* out) {
@@ -233,15 +232,15 @@ __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, 
         const uint32_t r = rr * PX + tr;
         const uint64_t o = obase + static_cast<uint64_t>(r) * kOut;
         if (q.flip)
-            emit_run<BF16, true, DBG>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
+            emit_run<BF16, true>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
         else
-            emit_run<BF16, false, DBG>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
+            emit_run<BF16, false>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
     }
 }
 
 // PX output pixels per thread: 4 (fp32, one float4 per plane) or 8 (bf16,
 // eight bf16 per plane).  kThreads/(224/PX) = PX rows per pass.
-template <bool BF16, int DBG = 0>
+template <bool BF16>
 // (measured: 4 resident CTAs per SM at 72 registers beat forcing 5-9 by
 // register caps or a larger shared-memory carveout; profiles/r01_augment_ab.md)
 __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
@@ -272,7 +271,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     const uint32_t a0 = (3 * q.x0) & ~15u;
     const uint32_t nch = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
     const uint8_t* gbase = src + static_cast<uint64_t>(q.y0 + band * kBand) * row_bytes + a0;
-    if (DBG != 1) {  // debug 1: no source loads
+    {
         // every load of the band in flight at once: slot t -> (row t/44, chunk t%44)
         constexpr uint32_t kSlots = kRowSmem / 16;  // 44 >= 43 chunks per row
         constexpr uint32_t kIters = (kBand * kSlots + kThreads - 1) / kThreads;
@@ -291,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     }
     __syncthreads();
 
-    emit_band<BF16, DBG>(&rows[0][0], q, a0, k, band, a.nc, a.out);
+    emit_band<BF16>(&rows[0][0], q, a0, k, band, a.nc, a.out);
 }
 
 // K7: variable geometry, bilinear resize (half-pixel centres, edge clamp).
@@ -489,17 +488,6 @@ NormConst norm_constants(const ll_augment_spec& s) {
     return c;
 }
 
-// Debug knob for measurements only (LL_AUG_DEBUG): 1 = skip source loads,
-// 2 = skip output stores.  Results are wrong by construction; never set in
-// product runs.
-static int crop_debug() {
-    static int v = [] {
-        const char* e = getenv("LL_AUG_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
 static void validate_spec(const ll_augment_spec& spec, uint32_t H, uint32_t W) {
     require(spec.out_dtype == LL_OUT_F32 || spec.out_dtype == LL_OUT_BF16,
             "augment: out_dtype must be fp32 or bf16");
@@ -532,15 +520,8 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
     const bool bf16 = spec.out_dtype == LL_OUT_BF16;
     if (spec.mode == LL_AUG_CROP) {
         const dim3 grid(static_cast<unsigned>(n * kBands));
-        const int dbg = crop_debug();
         launch(ctx, "augment_crop", [&] {
-            if (dbg == 1)
-                bf16 ? k_augment_crop<true, 1><<<grid, kThreads, 0, ctx->stream>>>(a)
-                     : k_augment_crop<false, 1><<<grid, kThreads, 0, ctx->stream>>>(a);
-            else if (dbg == 2)
-                bf16 ? k_augment_crop<true, 2><<<grid, kThreads, 0, ctx->stream>>>(a)
-                     : k_augment_crop<false, 2><<<grid, kThreads, 0, ctx->stream>>>(a);
-            else if (bf16)
+            if (bf16)
                 k_augment_crop<true><<<grid, kThreads, 0, ctx->stream>>>(a);
             else
                 k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);
