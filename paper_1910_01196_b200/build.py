@@ -16,6 +16,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "liblocload_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
+PER_FILE = {}
+
 SOURCES = ["capi.cu", "permute.cu", "assign.cu", "shard.cu", "augment.cu", "exchange.cu",
            "loader.cu", "host/locload_api.cpp"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
@@ -48,7 +50,8 @@ def build(force: bool = False, verbose: bool = False, extra=(), lib=None) -> str
     logs = []
     for src in SOURCES:
         obj = os.path.join(objdir, os.path.basename(src).rsplit(".", 1)[0] + ".o")
-        cmd = [NVCC, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *PER_FILE.get(src, []), *extra, "-c", os.path.join(CSRC, src), "-o",
+               obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stdout + r.stderr)
         if r.returncode != 0:
