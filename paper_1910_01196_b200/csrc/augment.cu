@@ -441,22 +441,21 @@ __global__ void __launch_bounds__(256) k_augment_resize_band(AugArgs a, const Re
     tap_y(oy0, &r_first, &t0, &tw);
     tap_y(oy0 + rows_out - 1, &t0, &r_last, &tw);
     const uint32_t nrows = r_last - r_first + 1;  // <= max_rows (host bound)
-    // stage the tapped source rows: bytes [x0*3, (x0+cw)*3) of each, 16-B aligned
-    const uint32_t nchunk = row_stride / 16;
-    for (uint32_t r = tid; r < nrows; r += blockDim.x) {
-        const uintptr_t g = reinterpret_cast<uintptr_t>(s_src) +
-                            static_cast<uint64_t>(q.y0 + r_first + r) * W * 3 + q.x0 * 3;
-        s_shift[r] = static_cast<uint32_t>(g & 15);
-    }
-    __syncthreads();
-    for (uint32_t t = tid; t < nrows * nchunk; t += blockDim.x) {
-        const uint32_t r = t / nchunk, c = t - r * nchunk;
-        const uintptr_t g = reinterpret_cast<uintptr_t>(s_src) +
-                            static_cast<uint64_t>(q.y0 + r_first + r) * W * 3 + q.x0 * 3;
-        const uintptr_t a16 = g & ~static_cast<uintptr_t>(15);
-        if (a16 + 16 * c < g + 3ull * q.cw)
-            *reinterpret_cast<uint4*>(rowbuf + r * row_stride + 16 * c) =
-                ld_nc_v4(reinterpret_cast<const void*>(a16 + 16 * c));
+    // stage the tapped source rows: bytes [x0*3, (x0+cw)*3) of each, 16-B
+    // aligned; one warp per row, lanes over 16-byte chunks
+    {
+        const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+        for (uint32_t r = warp; r < nrows; r += nwarps) {
+            const uintptr_t g = reinterpret_cast<uintptr_t>(s_src) +
+                                static_cast<uint64_t>(q.y0 + r_first + r) * W * 3 + q.x0 * 3;
+            const uintptr_t a16 = g & ~static_cast<uintptr_t>(15);
+            const uint32_t need = static_cast<uint32_t>((g + 3ull * q.cw - a16 + 15) / 16);
+            if (lane == 0) s_shift[r] = static_cast<uint32_t>(g - a16);
+            uint8_t* dst = rowbuf + r * row_stride;
+            for (uint32_t c = lane; c < need; c += 32)
+                *reinterpret_cast<uint4*>(dst + 16 * c) =
+                    ld_nc_v4(reinterpret_cast<const void*>(a16 + 16 * c));
+        }
     }
     __syncthreads();
     // row taps of the band, once
@@ -480,34 +479,40 @@ __global__ void __launch_bounds__(256) k_augment_resize_band(AugArgs a, const Re
         inv2[c] = pk(__float_as_uint(a.nc.inv_std255[c]), __float_as_uint(a.nc.inv_std255[c]));
     }
     const uint64_t big = 0x4B0000004B000000ull;  // {2^23, 2^23}
-    for (uint32_t task = tid; task < rows_out * pairs; task += blockDim.x) {
-        const uint32_t rr = task / pairs, ox = 2 * (task - rr * pairs), oy = oy0 + rr;
-        const uint8_t* r0 = rowbuf + s_y[rr][0];
-        const uint8_t* r1 = rowbuf + s_y[rr][1];
-        const uint32_t wyb = __float_as_uint(s_wy[rr]);
-        const uint64_t wy2 = pk(wyb, wyb);
+    // thread -> one output pixel pair (column taps loaded once), rows strided
+    const uint32_t groups = blockDim.x / pairs;
+    const uint32_t g0 = tid / pairs;
+    if (g0 < groups) {
+        const uint32_t ox = 2 * (tid - g0 * pairs);
         const uint64_t wx2 = pk(__float_as_uint(s_wx[ox]), __float_as_uint(s_wx[ox + 1]));
         const uint32_t pa0 = 3u * s_xlo[ox], pb0 = 3u * s_xhi[ox];
         const uint32_t pa1 = 3u * s_xlo[ox + 1], pb1 = 3u * s_xhi[ox + 1];
-        const uint64_t obase = k * 3 * plane + static_cast<uint64_t>(oy) * a.out_w + ox;
+        for (uint32_t rr = g0; rr < rows_out; rr += groups) {
+            const uint32_t oy = oy0 + rr;
+            const uint8_t* r0 = rowbuf + s_y[rr][0];
+            const uint8_t* r1 = rowbuf + s_y[rr][1];
+            const uint32_t wyb = __float_as_uint(s_wy[rr]);
+            const uint64_t wy2 = pk(wyb, wyb);
+            const uint64_t obase = k * 3 * plane + static_cast<uint64_t>(oy) * a.out_w + ox;
 #pragma unroll
-        for (uint32_t c = 0; c < 3; ++c) {
-            // 0x4B0000bb = 2^23 + bb: differences of these are exact byte
-            // differences, and (m - 2^23) is the byte itself -- the oracle's
-            // float arithmetic on packed fp32x2 lanes, no I2F
-            const uint64_t m00 = pk(0x4B000000u | r0[pa0 + c], 0x4B000000u | r0[pa1 + c]);
-            const uint64_t m01 = pk(0x4B000000u | r0[pb0 + c], 0x4B000000u | r0[pb1 + c]);
-            const uint64_t m10 = pk(0x4B000000u | r1[pa0 + c], 0x4B000000u | r1[pa1 + c]);
-            const uint64_t m11 = pk(0x4B000000u | r1[pb0 + c], 0x4B000000u | r1[pb1 + c]);
-            const uint64_t top = add2(sub2(m00, big), unfused(mul2(wx2, sub2(m01, m00)), a.zero));
-            const uint64_t bot = add2(sub2(m10, big), unfused(mul2(wx2, sub2(m11, m10)), a.zero));
-            const uint64_t v = add2(top, unfused(mul2(wy2, sub2(bot, top)), a.zero));
-            const uint64_t o = mul2(sub2(v, mean2[c]), inv2[c]);
-            const uint64_t idx = obase + c * plane;
-            if constexpr (BF16)
-                *reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(a.out) + idx) = bf16x2(o);
-            else
-                *reinterpret_cast<uint64_t*>(static_cast<float*>(a.out) + idx) = o;
+            for (uint32_t c = 0; c < 3; ++c) {
+                // 0x4B0000bb = 2^23 + bb: differences of these are exact byte
+                // differences, and (m - 2^23) is the byte itself -- the
+                // oracle's float arithmetic on packed fp32x2 lanes, no I2F
+                const uint64_t m00 = pk(0x4B000000u | r0[pa0 + c], 0x4B000000u | r0[pa1 + c]);
+                const uint64_t m01 = pk(0x4B000000u | r0[pb0 + c], 0x4B000000u | r0[pb1 + c]);
+                const uint64_t m10 = pk(0x4B000000u | r1[pa0 + c], 0x4B000000u | r1[pa1 + c]);
+                const uint64_t m11 = pk(0x4B000000u | r1[pb0 + c], 0x4B000000u | r1[pb1 + c]);
+                const uint64_t top = add2(sub2(m00, big), unfused(mul2(wx2, sub2(m01, m00)), a.zero));
+                const uint64_t bot = add2(sub2(m10, big), unfused(mul2(wx2, sub2(m11, m10)), a.zero));
+                const uint64_t v = add2(top, unfused(mul2(wy2, sub2(bot, top)), a.zero));
+                const uint64_t o = mul2(sub2(v, mean2[c]), inv2[c]);
+                const uint64_t idx = obase + c * plane;
+                if constexpr (BF16)
+                    *reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(a.out) + idx) = bf16x2(o);
+                else
+                    *reinterpret_cast<uint64_t*>(static_cast<float*>(a.out) + idx) = o;
+            }
         }
     }
 }
