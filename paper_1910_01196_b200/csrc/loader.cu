@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <tuple>
 #include <cstring>
 #include <vector>
 
@@ -58,6 +59,14 @@ struct ll_loader {
     // exchange
     ncclComm_t comm = nullptr;
     ll::DevBuf packbuf, recvbuf;
+    // NCCL exchange of step t+1 issued on the side stream while step t's
+    // augment runs (two buffer sets, alternating by step parity)
+    ll::DevBuf xpack[2], xrecv[2];
+    cudaEvent_t xdone[2] = {nullptr, nullptr}, augdone[2] = {nullptr, nullptr};
+    struct Pending {
+        bool valid = false;
+        uint64_t epoch = 0, step = 0;
+    } xpending[2];
     std::vector<void*> peer_open;  // opened IPC mappings (excluding self)
     ll::DevBuf d_peers;
     bool peers_ready = false;
@@ -143,9 +152,48 @@ void ensure_out(ll_loader* ld) {
 
 // Issue exchange + augment of one step whose plan tables are at (plan, step)
 // with host mirrors (h_*, index hs).
+// K5 pack + one grouped NCCL send/recv of step `step` on `stream`; received
+// samples land in `recv` in the learner's final-list order.
+void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_move* h_moves,
+                    uint32_t h_nmoves, const uint32_t* h_off, DevBuf& pack, DevBuf& recv,
+                    cudaStream_t stream) {
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const uint32_t me = c.rank;
+    require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
+    require(c.geometry == LL_GEOM_FIXED, "loader: variable-size samples need the P2P exchange");
+    const uint32_t* d_final_step = pd.final_ids + step * c.batch_size;
+    const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
+    uint64_t n_send = 0, n_recv = 0;
+    for (const ll_xfer& x : xs) (x.is_send ? n_send : n_recv) += x.count;
+    pack.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
+    recv.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
+    cudaStream_t main = ctx->stream;
+    ctx->stream = stream;  // pack_device launches on the context stream
+    try {
+        pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
+                    pack.as<uint8_t>());
+    } catch (...) {
+        ctx->stream = main;
+        throw;
+    }
+    ctx->stream = main;
+    LL_NCCL(ncclGroupStart());
+    for (const ll_xfer& x : xs) {
+        if (x.is_send)
+            LL_NCCL(ncclSend(pack.as<uint8_t>() + x.buf_first * ld->S, x.count * ld->S, ncclUint8,
+                             static_cast<int>(x.peer), ld->comm, stream));
+        else
+            LL_NCCL(ncclRecv(recv.as<uint8_t>() + x.buf_first * ld->S, x.count * ld->S, ncclUint8,
+                             static_cast<int>(x.peer), ld->comm, stream));
+    }
+    LL_NCCL(ncclGroupEnd());
+}
+
 void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
               const ll_move* h_moves, const uint32_t* h_off, const uint32_t* h_kept,
-              uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info) {
+              uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info,
+              const uint8_t* prefetched_recv = nullptr) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
@@ -186,27 +234,13 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
         n_recv = n_local;
     } else if (p > 1 && (n_send || n_recv)) {
         if (c.exchange == LL_EXCHANGE_NCCL) {
-            require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
-            require(c.geometry == LL_GEOM_FIXED,
-                    "loader: variable-size samples need the P2P exchange");
-            const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
-            ld->packbuf.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
-            ld->recvbuf.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
-            pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
-                        ld->packbuf.as<uint8_t>());
-            LL_NCCL(ncclGroupStart());
-            for (const ll_xfer& x : xs) {
-                if (x.is_send)
-                    LL_NCCL(ncclSend(ld->packbuf.as<uint8_t>() + x.buf_first * ld->S,
-                                     x.count * ld->S, ncclUint8, static_cast<int>(x.peer),
-                                     ld->comm, ctx->stream));
-                else
-                    LL_NCCL(ncclRecv(ld->recvbuf.as<uint8_t>() + x.buf_first * ld->S,
-                                     x.count * ld->S, ncclUint8, static_cast<int>(x.peer),
-                                     ld->comm, ctx->stream));
+            if (prefetched_recv) {
+                src.recv = prefetched_recv;
+            } else {
+                issue_exchange(ld, pd, step, h_moves, h_nmoves, h_off, ld->packbuf, ld->recvbuf,
+                               ctx->stream);
+                src.recv = ld->recvbuf.as<uint8_t>();
             }
-            LL_NCCL(ncclGroupEnd());
-            src.recv = ld->recvbuf.as<uint8_t>();
         } else if (c.exchange == LL_EXCHANGE_P2P) {
             require(ld->peers_ready, "loader: P2P exchange needs peer shards (open/link)");
             src.peers = ld->d_peers.as<const uint8_t*>();
@@ -378,6 +412,10 @@ void loader_destroy(ll_loader* ld) {
         if (h.done) cudaEventDestroy(h.done);
     }
     if (ld->side) cudaStreamDestroy(ld->side);
+    for (int i = 0; i < 2; ++i) {
+        if (ld->xdone[i]) cudaEventDestroy(ld->xdone[i]);
+        if (ld->augdone[i]) cudaEventDestroy(ld->augdone[i]);
+    }
     if (ld->storage) cudaFreeHost(ld->storage);
     if (ld->comm) ncclCommDestroy(ld->comm);
     delete ld;
@@ -495,6 +533,11 @@ uint64_t loader_steps(ll_loader* ld) { return ld->steps; }
 
 void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     set_device(ld->ctx);
+    // a prefetched exchange may still be packing from the old plan
+    for (int i = 0; i < 2; ++i) {
+        if (ld->xdone[i]) LL_CUDA(cudaStreamWaitEvent(ld->ctx->stream, ld->xdone[i], 0));
+        ld->xpending[i].valid = false;
+    }
     const ll_loader_config& c = ld->cfg;
     permute_device(ld->ctx, c.seed, epoch, static_cast<uint32_t>(c.d), ld->order.as<uint32_t>(),
                    nullptr, 0);
@@ -510,9 +553,61 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
     require(step < ld->steps, "Loader: step out of range");
     if (ld->plan_epoch != static_cast<int64_t>(epoch)) loader_plan_epoch(ld, epoch);
     set_device(ld->ctx);
-    run_step(ld, epoch, ld->plan.view(), step, &ld->h_moves[step * kMaxP],
-             &ld->h_off[step * (kMaxP + 1)], &ld->h_kept[step * kMaxP], ld->h_nmoves[step],
-             &ld->h_stats[step * 4], info);
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const bool nccl = c.learners > 1 && c.exchange == LL_EXCHANGE_NCCL &&
+                      c.scheme != LL_SCHEME_REGULAR;
+    auto tables = [&](uint64_t st) {
+        return std::make_tuple(&ld->h_moves[st * kMaxP], &ld->h_off[st * (kMaxP + 1)],
+                               &ld->h_kept[st * kMaxP], ld->h_nmoves[st], &ld->h_stats[st * 4]);
+    };
+    const uint8_t* pre = nullptr;
+    const uint32_t slot = step & 1;
+    if (nccl) {
+        if (!ld->xdone[0]) {
+            for (int i = 0; i < 2; ++i) {
+                LL_CUDA(cudaEventCreateWithFlags(&ld->xdone[i], cudaEventDisableTiming));
+                LL_CUDA(cudaEventCreateWithFlags(&ld->augdone[i], cudaEventDisableTiming));
+            }
+            if (!ld->side) LL_CUDA(cudaStreamCreateWithFlags(&ld->side, cudaStreamNonBlocking));
+        }
+        auto& pend = ld->xpending[slot];
+        if (pend.valid && pend.epoch == epoch && pend.step == step) {
+            LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
+        } else {
+            // not prefetched (first step of an epoch): exchange on the side
+            // stream into this slot's buffers, after the step that last read them
+            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[slot], 0));
+            auto [mv, off, kept, nm, st] = tables(step);
+            (void)kept;
+            (void)st;
+            issue_exchange(ld, ld->plan.view(), step, mv, nm, off, ld->xpack[slot],
+                           ld->xrecv[slot], ld->side);
+            LL_CUDA(cudaEventRecord(ld->xdone[slot], ld->side));
+            LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
+        }
+        pend.valid = false;
+        pre = ld->xrecv[slot].as<uint8_t>();
+    }
+    {
+        auto [mv, off, kept, nm, st] = tables(step);
+        run_step(ld, epoch, ld->plan.view(), step, mv, off, kept, nm, st, info, pre);
+    }
+    if (nccl) {
+        LL_CUDA(cudaEventRecord(ld->augdone[slot], ctx->stream));
+        if (step + 1 < ld->steps) {
+            // prefetch the next step's exchange while this augment runs
+            const uint32_t ns = (step + 1) & 1;
+            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[ns], 0));
+            auto [mv, off, kept, nm, st] = tables(step + 1);
+            (void)kept;
+            (void)st;
+            issue_exchange(ld, ld->plan.view(), step + 1, mv, nm, off, ld->xpack[ns],
+                           ld->xrecv[ns], ld->side);
+            LL_CUDA(cudaEventRecord(ld->xdone[ns], ld->side));
+            ld->xpending[ns] = {true, epoch, step + 1};
+        }
+    }
 }
 
 void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint64_t* host_batch) {
