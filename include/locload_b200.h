@@ -210,6 +210,13 @@ int ll_loader_link_peers(ll_loader* const* loaders, uint32_t n);
 /* Fill this learner's HBM shard (CacheDirectory block, sampling.cpp:19-25)
  * with the generate_dataset bytes -- the populated cache of epoch 0. */
 int ll_loader_populate(ll_loader* ld);
+/* Fill the shard (and, for alpha < 1, the host storage tier) from the
+ * reference's on-disk dataset: files <root>/%08llu.bin written by
+ * generate_dataset (pipeline.cpp:202-234), read by `threads` host threads
+ * (0 = all cores) through pinned staging.  Missing / short files fail with
+ * LL_ERR_RUNTIME and read_sample's messages ("sample N: cannot open PATH",
+ * "sample N: truncated file PATH (read X of Y bytes)", pipeline.cpp:110-126). */
+int ll_loader_populate_from_files(ll_loader* ld, const char* root, uint32_t threads);
 /* Fill the shard from host memory instead: owned_count(rank) samples. */
 int ll_loader_populate_from_host(ll_loader* ld, const uint8_t* host_samples);
 int ll_loader_shard_range(ll_loader* ld, uint64_t* first_id, uint64_t* count);

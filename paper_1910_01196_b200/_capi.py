@@ -108,6 +108,7 @@ PROTOTYPES = {
     "ll_loader_open_peers": (C.c_int, [C.c_void_p, u8p]),
     "ll_loader_populate": (C.c_int, [C.c_void_p]),
     "ll_loader_populate_from_host": (C.c_int, [C.c_void_p, u8p]),
+    "ll_loader_populate_from_files": (C.c_int, [C.c_void_p, C.c_char_p, C.c_uint32]),
     "ll_loader_shard_range": (C.c_int, [C.c_void_p, u64p, u64p]),
     "ll_loader_steps_per_epoch": (C.c_int, [C.c_void_p, u64p]),
     "ll_loader_plan_epoch": (C.c_int, [C.c_void_p, C.c_uint64]),

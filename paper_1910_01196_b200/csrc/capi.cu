@@ -23,6 +23,7 @@ void loader_open_peers(ll_loader* ld, const uint8_t* handles);
 void loader_populate(ll_loader* ld);
 void loader_link_peers(ll_loader* const* lds, uint32_t n);
 void loader_populate_from_host(ll_loader* ld, const uint8_t* host);
+void loader_populate_from_files(ll_loader* ld, const char* root, uint32_t threads);
 void loader_shard_range(ll_loader* ld, uint64_t* first, uint64_t* count);
 uint64_t loader_steps(ll_loader* ld);
 void loader_plan_epoch(ll_loader* ld, uint64_t epoch);
@@ -466,6 +467,9 @@ int ll_exchange_plan(const ll_move* moves, uint32_t n_moves, const uint64_t* fin
 
 int ll_loader_populate(ll_loader* ld) {
     return guarded([&] { loader_populate(ld); });
+}
+int ll_loader_populate_from_files(ll_loader* ld, const char* root, uint32_t threads) {
+    return guarded([&] { loader_populate_from_files(ld, root, threads); });
 }
 int ll_loader_populate_from_host(ll_loader* ld, const uint8_t* host_samples) {
     return guarded([&] { loader_populate_from_host(ld, host_samples); });

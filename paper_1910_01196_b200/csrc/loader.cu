@@ -17,6 +17,11 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <thread>
 #include <tuple>
 #include <cstring>
 #include <vector>
@@ -521,6 +526,140 @@ void loader_populate_from_host(ll_loader* ld, const uint8_t* host) {
     LL_CUDA(cudaMemcpyAsync(ld->shard.ptr, host, ld->owned * ld->S, cudaMemcpyHostToDevice,
                             ld->ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));
+    ld->populated = true;
+}
+
+// Cache population from the reference's on-disk dataset (generate_dataset /
+// sample_path: `<root>/%08llu.bin`, pipeline.cpp:202-234): the learner's
+// CacheDirectory block goes to its HBM shard and, for alpha < 1, ids
+// [cached, d) to the host storage tier.  `threads` host threads read files
+// into a pinned staging window that is copied to the device while the next
+// window is read.  Errors name the sample like read_sample (pipeline.cpp:110-126).
+namespace {
+
+std::string sample_file(const std::string& root, uint64_t id) {
+    char name[32];
+    std::snprintf(name, sizeof(name), "%08llu.bin", static_cast<unsigned long long>(id));
+    return root.empty() || root.back() == '/' ? root + name : root + "/" + name;
+}
+
+uint64_t sample_size(const ll_loader* ld, uint64_t id) {
+    if (ld->cfg.geometry == LL_GEOM_FIXED) return ld->S;
+    uint32_t h, w;
+    var_hw(ld->cfg.data_seed, id, &h, &w);
+    return 3ull * h * w;
+}
+
+// Reads ids [lo, hi) into dst (host) at offsets off(id); parallel over files.
+template <typename Off>
+void read_files(const ll_loader* ld, const std::string& root, uint64_t lo, uint64_t hi,
+                uint8_t* dst, Off off, uint32_t threads) {
+    std::atomic<uint64_t> next{lo};
+    std::mutex err_mu;
+    std::string err;
+    auto work = [&] {
+        for (;;) {
+            const uint64_t id = next.fetch_add(1);
+            if (id >= hi) return;
+            const std::string path = sample_file(root, id);
+            const uint64_t want = sample_size(ld, id);
+            FILE* f = std::fopen(path.c_str(), "rb");
+            std::string e;
+            if (!f) {
+                e = "sample " + std::to_string(id) + ": cannot open " + path;
+            } else {
+                const size_t got = std::fread(dst + off(id), 1, want, f);
+                std::fclose(f);
+                if (got != want)
+                    e = "sample " + std::to_string(id) + ": truncated file " + path + " (read " +
+                        std::to_string(got) + " of " + std::to_string(want) + " bytes)";
+            }
+            if (!e.empty()) {
+                std::lock_guard<std::mutex> g(err_mu);
+                if (err.empty()) err = e;
+                next.store(hi);
+                return;
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (uint32_t t = 1; t < threads; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    if (!err.empty()) fail(LL_ERR_RUNTIME, err);
+}
+
+} // namespace
+
+void loader_populate_from_files(ll_loader* ld, const char* root_c, uint32_t threads) {
+    require(root_c != nullptr, "Loader: null dataset root");
+    set_device(ld->ctx);
+    ll_ctx* ctx = ld->ctx;
+    const std::string root(root_c);
+    if (threads == 0) threads = std::max(1u, std::thread::hardware_concurrency());
+    const ll_loader_config& c = ld->cfg;
+    // HBM shard: windows of ~256 MiB through two pinned staging buffers
+    const uint64_t first = ld->first, end = ld->first + ld->owned;
+    std::vector<uint64_t> prefix;  // variable geometry: host copy of the shard's prefix
+    if (c.geometry == LL_GEOM_VARIABLE) {
+        prefix.resize(ld->owned + 1);
+        LL_CUDA(cudaMemcpy(prefix.data(), ld->prefix.as<uint64_t>() + first,
+                           sizeof(uint64_t) * (ld->owned + 1), cudaMemcpyDeviceToHost));
+    }
+    auto off_in_shard = [&](uint64_t id) -> uint64_t {
+        return c.geometry == LL_GEOM_FIXED ? (id - first) * ld->S : prefix[id - first] - prefix[0];
+    };
+    const uint64_t window = 256ull << 20;
+    uint8_t* stage[2] = {nullptr, nullptr};
+    cudaEvent_t copied[2] = {nullptr, nullptr};
+    try {
+        for (int i = 0; i < 2; ++i) {
+            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&stage[i]), window + (4ull << 20), 0));
+            LL_CUDA(cudaEventCreateWithFlags(&copied[i], cudaEventDisableTiming));
+        }
+        uint64_t id = first;
+        int b = 0;
+        while (id < end) {
+            // ids [id, stop) fit the window (at least one sample always)
+            uint64_t stop = id, bytes = 0;
+            while (stop < end) {
+                const uint64_t sz = off_in_shard(stop + 1) - off_in_shard(stop);  // padded size
+                if (bytes && bytes + sz > window) break;
+                bytes += sz;
+                ++stop;
+            }
+            LL_CUDA(cudaEventSynchronize(copied[b]));  // staging buffer b free again
+            const uint64_t base = off_in_shard(id);
+            read_files(ld, root, id, stop, stage[b],
+                       [&](uint64_t s) { return off_in_shard(s) - base; }, threads);
+            LL_CUDA(cudaMemcpyAsync(ld->shard.as<uint8_t>() + base, stage[b], bytes,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+            LL_CUDA(cudaEventRecord(copied[b], ctx->stream));
+            id = stop;
+            b ^= 1;
+        }
+        LL_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+        cudaStreamSynchronize(ctx->stream);
+        for (int i = 0; i < 2; ++i) {
+            if (stage[i]) cudaFreeHost(stage[i]);
+            if (copied[i]) cudaEventDestroy(copied[i]);
+        }
+        throw;
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaFreeHost(stage[i]);
+        cudaEventDestroy(copied[i]);
+    }
+    // storage tier: straight into the pinned host buffer
+    const uint64_t n_unc = c.d - ld->cached;
+    if (n_unc) {
+        if (!ld->storage)
+            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ld->storage), n_unc * ld->S,
+                                  cudaHostAllocMapped | cudaHostAllocPortable));
+        read_files(ld, root, ld->cached, c.d, ld->storage,
+                   [&](uint64_t s) { return (s - ld->cached) * ld->S; }, threads);
+    }
     ld->populated = true;
 }
 

@@ -140,6 +140,11 @@ class DeviceLoader:
     def populate(self) -> None:
         check(_capi.lib().ll_loader_populate(self._h))
 
+    def populate_from_files(self, root: str, threads: int = 0) -> None:
+        """Cache population from the reference's on-disk dataset
+        (<root>/%08llu.bin, generate_dataset); errors name the sample."""
+        check(_capi.lib().ll_loader_populate_from_files(self._h, root.encode(), threads))
+
     def populate_from_host(self, samples: np.ndarray) -> None:
         a = np.ascontiguousarray(samples, dtype=np.uint8)
         check(_capi.lib().ll_loader_populate_from_host(self._h, ptr(a, C.c_uint8)))

@@ -541,3 +541,76 @@ def test_loader_storage_tier_vs_oracle(p, alpha):
             for k, sid in enumerate(lst):
                 want = oracle.augment(src[k].reshape(256, 256, 3), int(sid), seed, 1)
                 assert np.array_equal(got[k], want), (t, j, k, int(sid) >= cached)
+
+
+def test_loader_populate_from_reference_files(tmp_path):
+    """Cache population from a dataset written by the REFERENCE's
+    generate_dataset (oracle/_ref): the learner serves exactly the oracle's
+    samples; missing and truncated files raise errors naming the sample like
+    read_sample (test_pipeline.cpp:177-192)."""
+    import os
+    d, p, B, seed = 600, 2, 64, 9
+    root = str(tmp_path / "ds")
+    oracle._ref_check(oracle.ref().ref_generate_dataset(root.encode(), d, 256 * 256 * 3, seed))
+    lds = []
+    for j in range(p):
+        ld = DeviceLoader(LoaderConfig(d=d, learners=p, rank=j, batch_size=B, seed=seed,
+                                       data_seed=seed, exchange="p2p"))
+        ld.populate_from_files(root, threads=4)
+        lds.append(ld)
+    DeviceLoader.link_peers(lds)
+    order = oracle.permute_epoch(seed, 0, d)
+    r = oracle.assign_step(order[:B], p, d, oracle.MODE_LOCALITY_BALANCED)
+    for j, ld in enumerate(lds):
+        info = ld.step(0, 0)
+        lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+        got = ld.fetch(info)
+        src = oracle.gen_samples(seed, lst, 256 * 256 * 3)
+        for k, sid in enumerate(lst):
+            assert np.array_equal(got[k], oracle.augment(src[k].reshape(256, 256, 3), int(sid), seed, 0))
+    os.remove(os.path.join(root, "00000017.bin"))
+    with open(os.path.join(root, "00000403.bin"), "wb") as f:
+        f.write(b"xy")
+    ld0 = DeviceLoader(LoaderConfig(d=d, learners=2, rank=0, batch_size=B))
+    with pytest.raises(RuntimeError, match="sample 17: cannot open"):
+        ld0.populate_from_files(root)
+    ld1 = DeviceLoader(LoaderConfig(d=d, learners=2, rank=1, batch_size=B))
+    with pytest.raises(RuntimeError, match=r"sample 403: truncated file .* \(read 2 of 196608 bytes\)"):
+        ld1.populate_from_files(root)
+
+
+def test_loader_populate_from_files_variable_and_storage(tmp_path):
+    """Variable-size files (cfg5 geometry) into the HBM shard, and alpha < 1
+    ids into the host storage tier."""
+    import os
+    d, B, seed = 300, 32, 5
+    root = str(tmp_path / "var")
+    os.makedirs(root)
+    for s in range(d):
+        h, w = oracle.sample_hw(seed, s)
+        with open(os.path.join(root, f"{s:08d}.bin"), "wb") as f:
+            f.write(oracle.gen_sample(seed, s, h * w * 3).tobytes())
+    ld = DeviceLoader(LoaderConfig(d=d, height=0, width=0, batch_size=B, seed=seed, data_seed=seed,
+                                   geometry="variable",
+                                   augment=AugmentConfig(mode="resize", out_dtype="bf16")))
+    ld.populate_from_files(root)
+    info = ld.step(1, 2)
+    lst = ld.fetch_ids(info)
+    got = ld.fetch(info)
+    for k, sid in enumerate(lst[:8]):
+        h, w = oracle.sample_hw(seed, int(sid))
+        src = oracle.gen_sample(seed, int(sid), h * w * 3).reshape(h, w, 3)
+        assert np.array_equal(got[k], oracle.augment(src, int(sid), seed, 1, mode=oracle.AUG_RESIZE,
+                                                     bf16=True))
+    # fixed-size files with a storage tier
+    root2 = str(tmp_path / "fix")
+    oracle._ref_check(oracle.ref().ref_generate_dataset(root2.encode(), d, 256 * 256 * 3, seed))
+    ld2 = DeviceLoader(LoaderConfig(d=d, batch_size=B, alpha=0.4, seed=seed, data_seed=seed))
+    ld2.populate_from_files(root2)
+    info = ld2.step(0, 1)
+    lst = ld2.fetch_ids(info)
+    got = ld2.fetch(info)
+    assert info.uncached > 0
+    src = oracle.gen_samples(seed, lst, 256 * 256 * 3)
+    for k, sid in enumerate(lst):
+        assert np.array_equal(got[k], oracle.augment(src[k].reshape(256, 256, 3), int(sid), seed, 0))
