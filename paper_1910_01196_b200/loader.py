@@ -218,6 +218,33 @@ class DeviceLoader:
                                                   info.device_out, out.nbytes))
         return out
 
+    def stream_ptr(self) -> int:
+        sp = C.c_size_t()
+        check(_capi.lib().ll_ctx_stream(self.ctx, C.byref(sp)))
+        return sp.value
+
+    def torch_batch(self, info: _capi.StepInfo):
+        """Zero-copy torch view of a step's augmented batch ([n, 3, H, W] on this
+        GPU; float32 or bfloat16) -- the trainer hand-off.  torch's current
+        stream is made to wait for the loader stream, so the tensor can be used
+        right away; it stays valid until prefetch_depth later steps."""
+        import torch
+        a = self.cfg.augment
+        shape = (int(info.n_local), 3, a.out_h, a.out_w)
+
+        class _View:  # __cuda_array_interface__ (v3) over the library's buffer
+            __cuda_array_interface__ = {
+                "shape": shape, "typestr": "<f4" if a.out_dtype == "fp32" else "<u2",
+                "data": (int(info.device_out), False), "version": 3, "strides": None}
+
+        dev = torch.device("cuda", self.device)
+        t = torch.as_tensor(_View(), device=dev)
+        if a.out_dtype == "bf16":
+            t = t.view(torch.bfloat16)
+        loader_stream = torch.cuda.ExternalStream(self.stream_ptr(), device=dev)
+        torch.cuda.current_stream(dev).wait_stream(loader_stream)
+        return t
+
     def fetch_ids(self, info: _capi.StepInfo) -> np.ndarray:
         out = np.empty(info.n_local, np.uint32)
         if info.n_local:

@@ -614,3 +614,29 @@ def test_loader_populate_from_files_variable_and_storage(tmp_path):
     src = oracle.gen_samples(seed, lst, 256 * 256 * 3)
     for k, sid in enumerate(lst):
         assert np.array_equal(got[k], oracle.augment(src[k].reshape(256, 256, 3), int(sid), seed, 0))
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_torch_handoff_zero_copy_train_step(dtype):
+    """Trainer hand-off: the step's batch as a zero-copy
+    torch tensor on the loader's GPU, ordered after the loader stream, equal
+    to the library's own copy, and usable by a training step."""
+    import torch
+    ld = make_learners(4096, 1, 128, dtype=dtype)[0]
+    info = ld.step(0, 3)
+    t = ld.torch_batch(info)
+    assert t.shape == (128, 3, 224, 224)
+    assert t.dtype == (torch.float32 if dtype == "fp32" else torch.bfloat16)
+    assert t.data_ptr() == info.device_out
+    host = ld.fetch(info)
+    if dtype == "fp32":
+        assert np.array_equal(t.cpu().numpy(), host)
+    else:
+        assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16), host)
+    net = torch.nn.Sequential(torch.nn.Conv2d(3, 8, 7, stride=4), torch.nn.ReLU(),
+                              torch.nn.AdaptiveAvgPool2d(1), torch.nn.Flatten(),
+                              torch.nn.Linear(8, 10)).cuda()
+    loss = net(t.float()).logsumexp(1).mean()
+    loss.backward()
+    assert torch.isfinite(loss).item()
+    assert all(p.grad is not None for p in net.parameters())
