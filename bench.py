@@ -64,6 +64,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--prefetch-depth", type=int, default=2,
+                    help="LoaderConfig::prefetch_depth (output ring / host steps in flight)")
     args = ap.parse_args()
     if args.dtype is None:
         args.dtype = "bf16" if args.workload == "cfg5" else "fp32"
@@ -284,7 +286,8 @@ def run_ours(args):
     cfg = LoaderConfig(d=d, height=H, width=W, learners=n, rank=rank, batch_size=B,
                        alpha=alpha_for(args, n), seed=SEED, data_seed=SEED,
                        scheme="regular" if args.workload == "cfg4" else "locality_balanced",
-                       exchange=args.exchange if n > 1 else "none", prefetch_depth=2,
+                       exchange=args.exchange if n > 1 else "none",
+                       prefetch_depth=args.prefetch_depth,
                        geometry="variable" if cfg5 else "fixed",
                        augment=AugmentConfig(mode="resize" if cfg5 else "crop",
                                              out_dtype=args.dtype))
@@ -431,7 +434,7 @@ def run_ours(args):
         e2e = {"value": sum_over_ranks(k_e2e * args.per_gpu_batch) / wall, "unit": "samples/s",
                "h2d_bytes_per_step": h2d // k_e2e, "d2h_bytes_per_step": d2h // k_e2e,
                "steps": k_e2e,
-               "path": "ll_loader_submit_host/wait_host, prefetch_depth 2: GlobalBatch ids "
+               "path": f"ll_loader_submit_host/wait_host, prefetch_depth {depth}: GlobalBatch ids "
                        "from host memory -> device assign/exchange/augment -> local ids + "
                        "step tables to host; ll_permute_epoch order D2H per epoch"}
 

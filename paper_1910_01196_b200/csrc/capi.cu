@@ -13,8 +13,6 @@
 
 namespace ll {
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
-uint32_t permute_rounds(ll_ctx* ctx);
-void permute_profile(ll_ctx* ctx, uint64_t* out6);
 void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg);
 void loader_destroy(ll_loader* ld);
 void loader_comm_init(ll_loader* ld, const uint8_t* id128);

@@ -105,8 +105,12 @@ void launch(ll_ctx* ctx, const char* name, F&& f) {
 void set_device(ll_ctx* ctx);
 
 // permute.cu: full permutation of [0,d) into d_order (u32), on ctx->stream.
+// `tag` names the scratch buffers (independent permutations may be in flight
+// on different streams of one context, e.g. the loader's next-epoch plan)
 void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint32_t* d_order,
-                    const uint64_t* host_forced, uint64_t n_forced);
+                    const uint64_t* host_forced, uint64_t n_forced, const char* tag = "perm");
+uint32_t permute_rounds(ll_ctx* ctx, const char* tag = "perm");
+void permute_profile(ll_ctx* ctx, uint64_t* out6, const char* tag = "perm");
 
 // assign.cu
 constexpr uint32_t kMaxP = 64;

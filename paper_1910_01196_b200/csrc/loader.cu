@@ -32,7 +32,6 @@
 namespace ll {
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
 void narrow_device(ll_ctx* ctx, const uint64_t* in, uint32_t* out, uint64_t n);
-uint32_t permute_rounds(ll_ctx* ctx);
 }
 
 #define LL_NCCL(x)                                                                        \
@@ -55,12 +54,25 @@ struct ll_loader {
     ll::DevBuf prefix;            // variable geometry: global padded-size prefix [d+1]
     uint8_t* storage = nullptr;   // alpha < 1: pinned+mapped host copy of ids [cached, d)
     std::vector<uint64_t> h_prefix_ends;  // prefix at first and first+owned
-    // epoch plan
-    ll::DevBuf order;
-    ll::PlanBufs plan;
+    // epoch plans: two slots, the current epoch's and the next one being
+    // prefetched on plan_stream (host tables in pinned memory)
+    struct PlanSlot {
+        ll::DevBuf order;
+        ll::PlanBufs plan;
+        int64_t epoch = -1;          // epoch held (or being computed)
+        cudaEvent_t ready = nullptr; // tables landed in host memory
+        ll_move* moves = nullptr;    // pinned host tables
+        uint32_t *off = nullptr, *kept = nullptr, *counts = nullptr, *nmoves = nullptr,
+                 *stats = nullptr;
+    } slot[2];
+    int cur = 0;
+    cudaStream_t plan_stream = nullptr;
     int64_t plan_epoch = -1;
-    std::vector<ll_move> h_moves;
-    std::vector<uint32_t> h_off, h_kept, h_counts, h_nmoves, h_stats;
+    ll::PlanBufs& plan() { return slot[cur].plan; }
+    // current epoch's host tables
+    ll_move* h_moves = nullptr;
+    uint32_t *h_off = nullptr, *h_kept = nullptr, *h_counts = nullptr, *h_nmoves = nullptr,
+             *h_stats = nullptr;
     // exchange
     ncclComm_t comm = nullptr;
     ll::DevBuf packbuf, recvbuf;
@@ -110,24 +122,48 @@ uint64_t out_elem_bytes(const ll_loader_config& c) {
     return c.augment.out_dtype == LL_OUT_BF16 ? 2 : 4;
 }
 
-void copy_tables(ll_loader* ld, const PlanBufs& plan, uint64_t steps) {
-    ll_ctx* ctx = ld->ctx;
-    ld->h_moves.resize(steps * kMaxP);
-    ld->h_off.resize(steps * (kMaxP + 1));
-    ld->h_kept.resize(steps * kMaxP);
-    ld->h_counts.resize(steps * kMaxP);
-    ld->h_nmoves.resize(steps);
-    ld->h_stats.resize(steps * 4);
+// Queue the D2H of slot `k`'s step tables on `stream` (pinned destination) and
+// mark the slot's ready event.
+void copy_tables(ll_loader* ld, int k, cudaStream_t stream) {
+    auto& sl = ld->slot[k];
+    const uint64_t steps = ld->steps;
+    const PlanBufs& plan = sl.plan;
     auto d2h = [&](void* dst, const DevBuf& b, size_t n) {
-        LL_CUDA(cudaMemcpyAsync(dst, b.ptr, n, cudaMemcpyDeviceToHost, ctx->stream));
+        LL_CUDA(cudaMemcpyAsync(dst, b.ptr, n, cudaMemcpyDeviceToHost, stream));
     };
-    d2h(ld->h_moves.data(), plan.moves, sizeof(ll_move) * steps * kMaxP);
-    d2h(ld->h_off.data(), plan.off, sizeof(uint32_t) * steps * (kMaxP + 1));
-    d2h(ld->h_kept.data(), plan.kept, sizeof(uint32_t) * steps * kMaxP);
-    d2h(ld->h_counts.data(), plan.counts, sizeof(uint32_t) * steps * kMaxP);
-    d2h(ld->h_nmoves.data(), plan.n_moves, sizeof(uint32_t) * steps);
-    d2h(ld->h_stats.data(), plan.stats, sizeof(uint32_t) * steps * 4);
-    LL_CUDA(cudaStreamSynchronize(ctx->stream));
+    d2h(sl.moves, plan.moves, sizeof(ll_move) * steps * kMaxP);
+    d2h(sl.off, plan.off, sizeof(uint32_t) * steps * (kMaxP + 1));
+    d2h(sl.kept, plan.kept, sizeof(uint32_t) * steps * kMaxP);
+    d2h(sl.counts, plan.counts, sizeof(uint32_t) * steps * kMaxP);
+    d2h(sl.nmoves, plan.n_moves, sizeof(uint32_t) * steps);
+    d2h(sl.stats, plan.stats, sizeof(uint32_t) * steps * 4);
+    LL_CUDA(cudaEventRecord(sl.ready, stream));
+}
+
+AugPlan aug_plan(const ll_loader* ld, uint64_t epoch);
+
+// Compute epoch `epoch`'s plan into slot k on `stream`: permutation (scratch
+// tagged per slot, so a prefetch and an API call never share buffers),
+// assignment, host tables.
+void plan_into(ll_loader* ld, int k, uint64_t epoch, cudaStream_t stream) {
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    auto& sl = ld->slot[k];
+    const char* tag = k ? "plan1" : "plan0";
+    cudaStream_t main = ctx->stream;
+    ctx->stream = stream;  // the device helpers launch on the context stream
+    try {
+        permute_device(ctx, c.seed, epoch, static_cast<uint32_t>(c.d), sl.order.as<uint32_t>(),
+                       nullptr, 0, tag);
+        assign_device(ctx, sl.order.as<uint32_t>(), ld->steps, c.batch_size, c.learners,
+                      ld->cached, c.scheme, sl.plan.view(), aug_plan(ld, epoch));
+        copy_tables(ld, k, stream);
+    } catch (...) {
+        ctx->stream = main;
+        throw;
+    }
+    ctx->stream = main;
+    sl.epoch = static_cast<int64_t>(epoch);
 }
 
 AugPlan aug_plan(const ll_loader* ld, uint64_t epoch) {
@@ -400,8 +436,18 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
         shard_bytes = ends[1] - ends[0];
     }
     ld->shard.reserve(std::max<uint64_t>(shard_bytes, 16));
-    ld->order.reserve(sizeof(uint32_t) * c.d);
-    ld->plan.reserve(ld->steps, c.batch_size);
+    for (auto& sl : ld->slot) {
+        sl.order.reserve(sizeof(uint32_t) * c.d);
+        sl.plan.reserve(ld->steps, c.batch_size);
+        const uint64_t st = std::max<uint64_t>(ld->steps, 1);
+        LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.moves), sizeof(ll_move) * st * kMaxP, 0));
+        LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.off), sizeof(uint32_t) * st * (kMaxP + 1), 0));
+        LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.kept), sizeof(uint32_t) * st * kMaxP, 0));
+        LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.counts), sizeof(uint32_t) * st * kMaxP, 0));
+        LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.nmoves), sizeof(uint32_t) * st, 0));
+        LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.stats), sizeof(uint32_t) * st * 4, 0));
+        LL_CUDA(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+    }
     *out = ld.release();
 }
 
@@ -422,6 +468,14 @@ void loader_destroy(ll_loader* ld) {
         if (ld->augdone[i]) cudaEventDestroy(ld->augdone[i]);
     }
     if (ld->storage) cudaFreeHost(ld->storage);
+    for (auto& sl : ld->slot) {
+        for (void* q : {static_cast<void*>(sl.moves), static_cast<void*>(sl.off),
+                        static_cast<void*>(sl.kept), static_cast<void*>(sl.counts),
+                        static_cast<void*>(sl.nmoves), static_cast<void*>(sl.stats)})
+            if (q) cudaFreeHost(q);
+        if (sl.ready) cudaEventDestroy(sl.ready);
+    }
+    if (ld->plan_stream) cudaStreamDestroy(ld->plan_stream);
     if (ld->comm) ncclCommDestroy(ld->comm);
     delete ld;
 }
@@ -670,21 +724,56 @@ void loader_shard_range(ll_loader* ld, uint64_t* first, uint64_t* count) {
 
 uint64_t loader_steps(ll_loader* ld) { return ld->steps; }
 
+// Make `epoch` the current plan: take the prefetched slot when it holds it
+// (waiting only for its tables), else compute it now on the loader stream.
 void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     set_device(ld->ctx);
+    ll_ctx* ctx = ld->ctx;
     // a prefetched exchange may still be packing from the old plan
     for (int i = 0; i < 2; ++i) {
-        if (ld->xdone[i]) LL_CUDA(cudaStreamWaitEvent(ld->ctx->stream, ld->xdone[i], 0));
+        if (ld->xdone[i]) LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[i], 0));
         ld->xpending[i].valid = false;
     }
-    const ll_loader_config& c = ld->cfg;
-    permute_device(ld->ctx, c.seed, epoch, static_cast<uint32_t>(c.d), ld->order.as<uint32_t>(),
-                   nullptr, 0);
-    assign_device(ld->ctx, ld->order.as<uint32_t>(), ld->steps, c.batch_size, c.learners,
-                  ld->cached, c.scheme, ld->plan.view(), aug_plan(ld, epoch));
-    copy_tables(ld, ld->plan, ld->steps);
-    permute_rounds(ld->ctx);  // raises if the kernel's round guard tripped
+    const int k = ld->plan_epoch >= 0 ? ld->cur ^ 1 : ld->cur;
+    auto& sl = ld->slot[k];
+    if (sl.epoch != static_cast<int64_t>(epoch) || ld->plan_epoch < 0) {
+        LL_CUDA(cudaEventSynchronize(sl.ready));  // any prefetch into this slot is done
+        plan_into(ld, k, epoch, ctx->stream);
+    } else {
+        LL_CUDA(cudaStreamWaitEvent(ctx->stream, sl.ready, 0));  // prefetched
+    }
+    LL_CUDA(cudaEventSynchronize(sl.ready));
+    permute_rounds(ctx, k ? "plan1" : "plan0");  // raises if the round guard tripped
+    ld->cur = k;
+    ld->h_moves = sl.moves;
+    ld->h_off = sl.off;
+    ld->h_kept = sl.kept;
+    ld->h_counts = sl.counts;
+    ld->h_nmoves = sl.nmoves;
+    ld->h_stats = sl.stats;
     ld->plan_epoch = static_cast<int64_t>(epoch);
+}
+
+// Start planning epoch + 1 into the other slot on plan_stream, after
+// everything already issued on the loader stream (which includes every step
+// that read that slot's previous plan).
+void prefetch_plan(ll_loader* ld, uint64_t next_epoch) {
+    ll_ctx* ctx = ld->ctx;
+    const int k = ld->cur ^ 1;
+    auto& sl = ld->slot[k];
+    if (sl.epoch == static_cast<int64_t>(next_epoch)) return;
+    if (!ld->plan_stream) {
+        // highest priority: the permutation is a cooperative launch, and its
+        // blocks must win SMs back from the running augment grids promptly
+        int lo = 0, hi = 0;
+        LL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LL_CUDA(cudaStreamCreateWithPriority(&ld->plan_stream, cudaStreamNonBlocking, hi));
+    }
+    cudaEvent_t issued = ctx->take_event();
+    LL_CUDA(cudaEventRecord(issued, ctx->stream));
+    LL_CUDA(cudaStreamWaitEvent(ld->plan_stream, issued, 0));
+    ctx->event_pool.push_back(issued);
+    plan_into(ld, k, next_epoch, ld->plan_stream);
 }
 
 void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* info) {
@@ -720,7 +809,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             auto [mv, off, kept, nm, st] = tables(step);
             (void)kept;
             (void)st;
-            issue_exchange(ld, ld->plan.view(), step, mv, nm, off, ld->xpack[slot],
+            issue_exchange(ld, ld->plan().view(), step, mv, nm, off, ld->xpack[slot],
                            ld->xrecv[slot], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[slot], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
@@ -730,8 +819,10 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
     }
     {
         auto [mv, off, kept, nm, st] = tables(step);
-        run_step(ld, epoch, ld->plan.view(), step, mv, off, kept, nm, st, info, pre);
+        run_step(ld, epoch, ld->plan().view(), step, mv, off, kept, nm, st, info, pre);
     }
+    // halfway through the epoch, start the next epoch's plan on its own stream
+    if (step == ld->steps / 2) prefetch_plan(ld, epoch + 1);
     if (nccl) {
         LL_CUDA(cudaEventRecord(ld->augdone[slot], ctx->stream));
         if (step + 1 < ld->steps) {
@@ -741,7 +832,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             auto [mv, off, kept, nm, st] = tables(step + 1);
             (void)kept;
             (void)st;
-            issue_exchange(ld, ld->plan.view(), step + 1, mv, nm, off, ld->xpack[ns],
+            issue_exchange(ld, ld->plan().view(), step + 1, mv, nm, off, ld->xpack[ns],
                            ld->xrecv[ns], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[ns], ld->side));
             ld->xpending[ns] = {true, epoch, step + 1};
@@ -895,7 +986,7 @@ void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_
     const uint64_t B = ld->cfg.batch_size;
     const uint32_t p = ld->cfg.learners;
     std::vector<uint32_t> ids(B);
-    LL_CUDA(cudaMemcpy(ids.data(), ld->plan.final_ids.as<uint32_t>() + step * B,
+    LL_CUDA(cudaMemcpy(ids.data(), ld->plan().final_ids.as<uint32_t>() + step * B,
                        sizeof(uint32_t) * B, cudaMemcpyDeviceToHost));
     for (uint64_t i = 0; i < B; ++i) final_ids[i] = ids[i];
     for (uint32_t j = 0; j <= p; ++j) final_off[j] = ld->h_off[step * (kMaxP + 1) + j];

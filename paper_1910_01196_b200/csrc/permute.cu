@@ -372,12 +372,13 @@ __global__ void k_widen(const uint32_t* __restrict__ in, uint64_t* __restrict__ 
 } // namespace
 
 void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint32_t* d_order,
-                    const uint64_t* host_forced, uint64_t n_forced) {
-    DevBuf& J = ctx->buf("perm.J", sizeof(uint32_t) * d);
-    DevBuf& R = ctx->buf("perm.R", sizeof(unsigned long long) * d);
-    DevBuf& L0 = ctx->buf("perm.L0", sizeof(uint2) * d);
-    DevBuf& L1 = ctx->buf("perm.L1", sizeof(uint2) * d);
-    DevBuf& ctl = ctx->buf("perm.ctl", 128);
+                    const uint64_t* host_forced, uint64_t n_forced, const char* tag) {
+    const std::string t(tag);
+    DevBuf& J = ctx->buf(t + ".J", sizeof(uint32_t) * d);
+    DevBuf& R = ctx->buf(t + ".R", sizeof(unsigned long long) * d);
+    DevBuf& L0 = ctx->buf(t + ".L0", sizeof(uint2) * d);
+    DevBuf& L1 = ctx->buf(t + ".L1", sizeof(uint2) * d);
+    DevBuf& ctl = ctx->buf(t + ".ctl", 128);
     unsigned int init[16] = {kNone, kNone, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     LL_CUDA(cudaMemcpyAsync(ctl.ptr, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
     PermArgs a{};
@@ -392,7 +393,7 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
     a.shift = reinterpret_cast<unsigned long long*>(ctl.as<unsigned int>() + 8);
     a.n_forced = static_cast<uint32_t>(n_forced);
     if (n_forced) {
-        DevBuf& forced = ctx->buf("perm.forced", sizeof(uint64_t) * n_forced);
+        DevBuf& forced = ctx->buf(t + ".forced", sizeof(uint64_t) * n_forced);
         LL_CUDA(cudaMemcpyAsync(forced.ptr, host_forced, sizeof(uint64_t) * n_forced,
                                 cudaMemcpyHostToDevice, ctx->stream));
         LL_CUDA(cudaStreamSynchronize(ctx->stream));  // host_forced may be pageable
@@ -417,9 +418,10 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
     });
 }
 
-uint32_t permute_rounds(ll_ctx* ctx) {
+uint32_t permute_rounds(ll_ctx* ctx, const char* tag) {
+    const std::string t(tag);
     unsigned int ctl[2] = {0, 0};
-    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf("perm.ctl", 128).as<unsigned int>() + 2, sizeof(ctl),
+    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf(t + ".ctl", 128).as<unsigned int>() + 2, sizeof(ctl),
                             cudaMemcpyDeviceToHost, ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctl[1] != 0) fail(LL_ERR_RUNTIME, "permute: round limit exceeded (internal error)");
@@ -432,9 +434,10 @@ void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n) {
 }
 
 // {rounds, grid-wide rounds, ns draws+repair, ns grid rounds, ns CTA-0 rounds, ns total}
-void permute_profile(ll_ctx* ctx, uint64_t* out6) {
+void permute_profile(ll_ctx* ctx, uint64_t* out6, const char* tag) {
+    const std::string t(tag);
     unsigned int ctl[32];
-    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf("perm.ctl", 128).ptr, sizeof(ctl),
+    LL_CUDA(cudaMemcpyAsync(ctl, ctx->buf(t + ".ctl", 128).ptr, sizeof(ctl),
                             cudaMemcpyDeviceToHost, ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
     const uint64_t* ts = reinterpret_cast<const uint64_t*>(ctl + 16);
