@@ -153,6 +153,14 @@ typedef struct ll_augment_spec {
 int ll_augment(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, uint64_t epoch,
                const uint8_t* host_src, const uint64_t* host_ids, uint64_t n, uint32_t height,
                uint32_t width, void* host_out);
+/* The same on device buffers (asynchronous on the context stream): n samples
+ * at device_src + k*height*width*3 -- which may be a peer GPU's memory after
+ * ll_ctx_enable_peer -- with ids device_ids[k], into device_out. */
+int ll_augment_device(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, uint64_t epoch,
+                      uintptr_t device_src, uintptr_t device_ids, uint64_t n, uint32_t height,
+                      uint32_t width, uintptr_t device_out);
+/* let kernels of this context read `peer_device`'s memory (NVLink P2P) */
+int ll_ctx_enable_peer(ll_ctx* ctx, int peer_device);
 /* crop/flip parameters the augment uses (y0, x0, ch, cw, flip per sample) */
 int ll_augment_params(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, uint64_t epoch,
                       const uint64_t* host_ids, uint64_t n, uint32_t height, uint32_t width,

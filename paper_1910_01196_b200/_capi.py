@@ -97,6 +97,10 @@ PROTOTYPES = {
                                       u8p]),
     "ll_augment": (C.c_int, [C.c_void_p, C.POINTER(AugmentSpec), C.c_uint64, C.c_uint64, u8p,
                              u64p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "ll_augment_device": (C.c_int, [C.c_void_p, C.POINTER(AugmentSpec), C.c_uint64, C.c_uint64,
+                                    C.c_size_t, C.c_size_t, C.c_uint64, C.c_uint32, C.c_uint32,
+                                    C.c_size_t]),
+    "ll_ctx_enable_peer": (C.c_int, [C.c_void_p, C.c_int]),
     "ll_augment_params": (C.c_int, [C.c_void_p, C.POINTER(AugmentSpec), C.c_uint64, C.c_uint64,
                                     u64p, C.c_uint64, C.c_uint32, C.c_uint32, u32p]),
     "ll_loader_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_void_p,

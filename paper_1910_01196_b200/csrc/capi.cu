@@ -403,6 +403,38 @@ int ll_augment(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, uint64_t
     });
 }
 
+int ll_augment_device(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, uint64_t epoch,
+                      uintptr_t device_src, uintptr_t device_ids, uint64_t n, uint32_t height,
+                      uint32_t width, uintptr_t device_out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(spec != nullptr, "augment: null spec");
+        if (n == 0) return;
+        SrcMap m;
+        m.kind = 0;
+        m.base = reinterpret_cast<const uint8_t*>(device_src);
+        m.ids = reinterpret_cast<const uint64_t*>(device_ids);
+        m.sample_bytes = static_cast<uint64_t>(height) * width * 3;
+        augment_device(ctx, *spec, seed, epoch, m, n, height, width,
+                       reinterpret_cast<void*>(device_out));
+    });
+}
+
+int ll_ctx_enable_peer(ll_ctx* ctx, int peer_device) {
+    return guarded([&] {
+        check_ctx(ctx);
+        int can = 0;
+        LL_CUDA(cudaDeviceCanAccessPeer(&can, ctx->device, peer_device));
+        if (!can) fail(LL_ERR_UNSUPPORTED, "no peer access between these devices");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+            cudaGetLastError();
+            return;
+        }
+        LL_CUDA(e);
+    });
+}
+
 int ll_augment_params(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, uint64_t epoch,
                       const uint64_t* host_ids, uint64_t n, uint32_t height, uint32_t width,
                       uint32_t* host_params5) {
