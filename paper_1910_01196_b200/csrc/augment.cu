@@ -588,14 +588,8 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
         const uint32_t row_stride = ((3 * max_w + 15) / 16 + 1) * 16;
         const size_t smem = static_cast<size_t>(max_rows) * row_stride;
         if (spec.out_w % 2 == 0 && spec.out_w <= kMaxOutW && max_rows <= 64 && smem <= 160 * 1024) {
-            static bool attr = false;
-            if (!attr) {
-                LL_CUDA(cudaFuncSetAttribute(k_augment_resize_band<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-                LL_CUDA(cudaFuncSetAttribute(k_augment_resize_band<true>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-                attr = true;
-            }
+            ensure_smem_attr(k_augment_resize_band<false>, ctx->device, smem);
+            ensure_smem_attr(k_augment_resize_band<true>, ctx->device, smem);
             DevBuf& items = ctx->buf("resize.items", sizeof(ResizeItem) * n);
             launch(ctx, "resize_prep", [&] {
                 k_resize_prep<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(

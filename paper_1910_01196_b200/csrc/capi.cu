@@ -293,8 +293,7 @@ int ll_assign(ll_ctx* ctx, const uint64_t* host_batch, uint64_t B, uint64_t d, u
         const uint64_t Bs = B ? B : 1;
         DevBuf& b64 = ctx->buf("api.batch64", sizeof(uint64_t) * Bs);
         DevBuf& b32 = ctx->buf("api.batch32", sizeof(uint32_t) * Bs);
-        static thread_local std::map<ll_ctx*, std::unique_ptr<PlanBufs>> plans;
-        auto& pb = plans[ctx];
+        auto& pb = ctx->api_plan;
         if (!pb) pb.reset(new PlanBufs());
         pb->reserve(1, Bs);
         h2d(ctx, b64.ptr, host_batch, sizeof(uint64_t) * B);

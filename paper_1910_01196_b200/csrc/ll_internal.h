@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -54,6 +55,8 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
+struct PlanBufs;
+
 struct KernelTimes {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     uint64_t launches = 0;
@@ -79,9 +82,26 @@ struct ll_ctx {
         return *p;
     }
     cudaEvent_t take_event();
+    // single-step plan of the stateless ll_assign entry point
+    std::unique_ptr<ll::PlanBufs> api_plan;
 };
 
 namespace ll {
+
+// cudaFuncSetAttribute is per device: set a kernel's dynamic shared-memory
+// limit once per (kernel, device).
+template <typename K>
+void ensure_smem_attr(K kernel, int device, size_t bytes) {
+    static std::map<std::pair<const void*, int>, size_t> done;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> g(mu);
+    auto& v = done[{reinterpret_cast<const void*>(kernel), device}];
+    if (v >= bytes) return;
+    cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(bytes)),
+               "cudaFuncSetAttribute");
+    v = bytes;
+}
 
 // Every kernel launch of the library goes through here: counts it, and when
 // timing is on brackets it with events on the context stream.

@@ -399,12 +399,7 @@ void permute_device(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint32_t d, uint
         LL_CUDA(cudaStreamSynchronize(ctx->stream));  // host_forced may be pageable
         a.forced = forced.as<uint64_t>();
     }
-    static bool attr = false;
-    if (!attr) {
-        LL_CUDA(cudaFuncSetAttribute(k_permute, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(kTailSmem)));
-        attr = true;
-    }
+    ensure_smem_attr(k_permute, ctx->device, kTailSmem);
     int per_sm = 0;
     LL_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_permute, kThreads, kTailSmem));
     if (per_sm < 1) fail(LL_ERR_CUDA, "permute: kernel cannot be resident");
