@@ -287,6 +287,22 @@ static inline void store_px(void* out, uint64_t idx, float v, int out_bf16) {
     else ((float*)out)[idx] = v;
 }
 
+void lo_resize_tap(uint32_t o, uint32_t n_out, uint32_t extent, uint32_t* lo, uint32_t* w) {
+    /* f = 128 * ((o + 0.5) * extent / n_out - 0.5), floored, in exact integers */
+    const int64_t f = (int64_t)(((uint64_t)(2 * o + 1) * extent * 64) / n_out) - 64;
+    uint32_t l = 0, ww = 0;
+    if (f > 0) {
+        l = (uint32_t)(f >> 7);
+        ww = (uint32_t)(f & 127);
+    }
+    if (l >= extent - 1) {
+        l = extent - 1;
+        ww = 0;
+    }
+    *lo = l;
+    *w = ww;
+}
+
 void lo_augment_one(const uint8_t* src, uint32_t H, uint32_t W, const lo_aug_params* prm,
                     uint32_t out_h, uint32_t out_w, int mode, const float mean255[3],
                     const float inv_std255[3], int out_bf16, void* out) {
@@ -306,48 +322,39 @@ void lo_augment_one(const uint8_t* src, uint32_t H, uint32_t W, const lo_aug_par
         }
         return;
     }
-    /* RESIZE: bilinear, half-pixel centres, edge clamp.  Column taps are
-     * tabulated once per sample (same arithmetic, evaluated once). */
-    const float sy = (float)prm->ch / (float)out_h;
-    const float sx = (float)prm->cw / (float)out_w;
-    uint32_t* txa = (uint32_t*)malloc(sizeof(uint32_t) * out_w * 2);
-    float* twx = (float*)malloc(sizeof(float) * out_w);
+    /* RESIZE: fixed-point bilinear.  Source positions
+     * in 1/128 px, half-pixel centres, edge clamp; the four tap weights are
+     * products of 7-bit axis weights, so v is an exact integer < 2^22 and
+     * out = (v * 2^-14 - mean255) * inv_std255.  Column taps are tabulated
+     * once per sample. */
+    uint32_t* txl = (uint32_t*)malloc(sizeof(uint32_t) * out_w);
+    uint32_t* txw = (uint32_t*)malloc(sizeof(uint32_t) * out_w);
     for (uint32_t ox = 0; ox < out_w; ++ox) {
         const uint32_t mx = prm->flip ? out_w - 1 - ox : ox;
-        float fx = ((float)mx + 0.5f) * sx - 0.5f;
-        if (fx < 0.f) fx = 0.f;
-        uint32_t xlo = (uint32_t)fx;
-        if (xlo > prm->cw - 1) xlo = prm->cw - 1;
-        const uint32_t xhi = xlo + 1 < prm->cw ? xlo + 1 : prm->cw - 1;
-        twx[ox] = fx - (float)xlo;
-        txa[2 * ox] = (prm->x0 + xlo) * 3;
-        txa[2 * ox + 1] = (prm->x0 + xhi) * 3;
+        lo_resize_tap(mx, out_w, prm->cw, &txl[ox], &txw[ox]);
     }
     for (uint32_t oy = 0; oy < out_h; ++oy) {
-        float fy = ((float)oy + 0.5f) * sy - 0.5f;
-        if (fy < 0.f) fy = 0.f;
-        uint32_t ylo = (uint32_t)fy;
-        if (ylo > prm->ch - 1) ylo = prm->ch - 1;
-        const uint32_t yhi = ylo + 1 < prm->ch ? ylo + 1 : prm->ch - 1;
-        const float wy = fy - (float)ylo;
+        uint32_t ylo, wy;
+        lo_resize_tap(oy, out_h, prm->ch, &ylo, &wy);
+        const uint32_t yhi = wy ? ylo + 1 : ylo;
         const uint8_t* r0 = src + ((uint64_t)(prm->y0 + ylo) * W) * 3;
         const uint8_t* r1 = src + ((uint64_t)(prm->y0 + yhi) * W) * 3;
         for (uint32_t ox = 0; ox < out_w; ++ox) {
-            const float wx = twx[ox];
-            const uint64_t a = txa[2 * ox], b = txa[2 * ox + 1];
+            const uint32_t wx = txw[ox];
+            const uint64_t a = (uint64_t)(prm->x0 + txl[ox]) * 3;
+            const uint64_t b = wx ? a + 3 : a;
+            const uint32_t w00 = (128 - wx) * (128 - wy), w01 = wx * (128 - wy);
+            const uint32_t w10 = (128 - wx) * wy, w11 = wx * wy;
             for (int c = 0; c < 3; ++c) {
-                const float p00 = (float)r0[a + c], p01 = (float)r0[b + c];
-                const float p10 = (float)r1[a + c], p11 = (float)r1[b + c];
-                const float top = p00 + wx * (p01 - p00);
-                const float bot = p10 + wx * (p11 - p10);
-                const float v = top + wy * (bot - top);
-                const float o = (v - mean255[c]) * inv_std255[c];
+                const uint32_t v = w00 * r0[a + c] + w01 * r0[b + c] + w10 * r1[a + c] +
+                                   w11 * r1[b + c];
+                const float o = ((float)v * 0x1p-14f - mean255[c]) * inv_std255[c];
                 store_px(out, c * plane + (uint64_t)oy * out_w + ox, o, out_bf16);
             }
         }
     }
-    free(txa);
-    free(twx);
+    free(txl);
+    free(txw);
 }
 
 typedef struct {

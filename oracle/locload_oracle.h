@@ -115,6 +115,13 @@ void lo_norm_constants(const double mean[3], const double std_[3], float mean255
 
 uint16_t lo_bf16_rne(float f);
 
+/* RESIZE source tap along one axis: output index o of n_out over a crop of
+ * `extent` source pixels.  f = floor((2o+1)*extent*64 / n_out) - 64 (the
+ * half-pixel-centre position in 1/128 px), clamped at 0; lo = f >> 7,
+ * w = f & 127; at the far edge (lo >= extent-1) lo = extent-1 and w = 0.
+ * The second tap is lo+1 (weight w), used only when w > 0. */
+void lo_resize_tap(uint32_t o, uint32_t n_out, uint32_t extent, uint32_t* lo, uint32_t* w);
+
 /* src is HWC u8 (H x W x 3).  out is CHW (3 x out_h x out_w), fp32 when
  * out_bf16 == 0, else bf16 bits (uint16). */
 void lo_augment_one(const uint8_t* src, uint32_t H, uint32_t W, const lo_aug_params* prm,

@@ -22,7 +22,9 @@
 
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cmath>
+#include <type_traits>
 #include <cstdlib>
 
 namespace ll {
@@ -36,7 +38,6 @@ constexpr uint32_t kThreads = 224;
 
 struct AugArgs {
     SrcMap src;
-    uint32_t zero;  // always 0; see unfused()
     uint32_t H, W;
     uint64_t seed, epoch;
     NormConst nc;
@@ -107,16 +108,6 @@ __device__ __forceinline__ Params aug_params(uint64_t seed, uint64_t epoch, uint
     return q;
 }
 
-__device__ __forceinline__ float norm(uint32_t v, float mean, float inv) {
-    return __fmul_rn(__fsub_rn(static_cast<float>(v), mean), inv);
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    const __nv_bfloat16 a = __float2bfloat16_rn(lo), b = __float2bfloat16_rn(hi);
-    return static_cast<uint32_t>(__bfloat16_as_ushort(a)) |
-           (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
-}
-
 // Packed fp32x2 helpers (FADD2 / FMUL2 on sm_100): two IEEE-rounded ops per
 // instruction, bit-identical to the scalar sequence.
 __device__ __forceinline__ uint64_t pk(uint32_t lo, uint32_t hi) {
@@ -134,18 +125,7 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-    uint64_t r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
 __device__ __forceinline__ uint32_t lo32(uint64_t v) { return static_cast<uint32_t>(v); }
-// ptxas contracts mul.rn.f32x2 + add.rn.f32x2 into FFMA2 (one rounding
-// instead of two), which the oracle does not do.  XOR-ing the product with a
-// launch argument that is always zero makes it opaque and keeps both roundings.
-__device__ __forceinline__ uint64_t unfused(uint64_t prod, uint32_t zero) {
-    return prod ^ (static_cast<uint64_t>(zero) << 32 | zero);
-}
 __device__ __forceinline__ uint32_t hi32(uint64_t v) { return static_cast<uint32_t>(v >> 32); }
 
 // float(byte j of w) - 2^23 == byte exactly: PRMT builds 0x4B0000bb (2^23 + bb).
@@ -305,8 +285,45 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     emit_band<BF16>(&rows[0][0], q, a0, k, band, a.nc, a.out);
 }
 
-// K7: variable geometry, bilinear resize (half-pixel centres, edge clamp).
-// One CTA per (sample, output row); generic and straightforward (cfg5).
+// ---- K7: fixed-point bilinear resize (cfg5) ------------------------------
+// Semantics (oracle lo_resize_tap / lo_augment_one):
+// source positions in 1/128 px with half-pixel centres; each tap weight is a
+// product of 7-bit axis weights, so per channel
+//   v = sum (128-wy | wy) * (128-wx | wx) * p      (exact integer < 2^22)
+//   out = (v * 2^-14 - mean255) * inv_std255.
+// On the device the horizontal pair of taps of one source row is one DP2A
+// (two u16 weights x two u8 pixels), the vertical weight is folded into the
+// packed u16 weight pair (lanes <= 128*128, no carry), and v * 2^-14 is
+// exact through the magic float 0x44000000 | v (= 512 + v * 2^-14): the
+// whole tap arithmetic runs on the integer pipes and no float rounding
+// happens before the normalisation.
+
+// U = uint32_t when (2*n_out+1)*extent*64 < 2^32 (the banded kernel; host
+// checked), else uint64_t: the same floor either way.
+template <typename U = uint64_t>
+__device__ __forceinline__ void resize_tap(uint32_t o, uint32_t n_out, uint32_t extent,
+                                           uint32_t* lo, uint32_t* w) {
+    const int64_t f = static_cast<int64_t>((static_cast<U>(2 * o + 1) * extent * 64) / n_out) - 64;
+    uint32_t l = 0, ww = 0;
+    if (f > 0) {
+        l = static_cast<uint32_t>(f >> 7);
+        ww = static_cast<uint32_t>(f & 127);
+    }
+    if (l >= extent - 1) {
+        l = extent - 1;
+        ww = 0;
+    }
+    *lo = l;
+    *w = ww;
+}
+
+// v * 2^-14 as an exact float (v < 2^22)
+__device__ __forceinline__ float fixed14(uint32_t v) {
+    return __fsub_rn(__uint_as_float(0x44000000u | v), 512.0f);
+}
+
+// K7 generic: one CTA per (sample, output row), scalar; used outside the
+// banded kernel's limits (out_w > 512, sources of 2 GiB+ or under 2 x 2).
 template <bool BF16>
 __global__ void __launch_bounds__(256) k_augment_resize(AugArgs a) {
     const uint64_t k = blockIdx.x / a.out_h;
@@ -322,34 +339,23 @@ __global__ void __launch_bounds__(256) k_augment_resize(AugArgs a) {
     }
     __syncthreads();
     const Params q = s_prm;
-    const uint8_t* src = s_src;
-    const float sy = __fdiv_rn(static_cast<float>(q.ch), static_cast<float>(a.out_h));
-    const float sx = __fdiv_rn(static_cast<float>(q.cw), static_cast<float>(a.out_w));
-    float fy = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(oy), 0.5f), sy), 0.5f);
-    if (fy < 0.f) fy = 0.f;
-    uint32_t ylo = static_cast<uint32_t>(fy);
-    if (ylo > q.ch - 1) ylo = q.ch - 1;
-    const uint32_t yhi = ylo + 1 < q.ch ? ylo + 1 : q.ch - 1;
-    const float wy = __fsub_rn(fy, static_cast<float>(ylo));
-    const uint8_t* r0 = src + static_cast<uint64_t>(q.y0 + ylo) * a.W * 3;
-    const uint8_t* r1 = src + static_cast<uint64_t>(q.y0 + yhi) * a.W * 3;
+    uint32_t ylo, wy;
+    resize_tap(oy, a.out_h, q.ch, &ylo, &wy);
+    const uint32_t yhi = wy ? ylo + 1 : ylo;
+    const uint8_t* r0 = s_src + static_cast<uint64_t>(q.y0 + ylo) * a.W * 3;
+    const uint8_t* r1 = s_src + static_cast<uint64_t>(q.y0 + yhi) * a.W * 3;
     const uint64_t plane = static_cast<uint64_t>(a.out_h) * a.out_w;
     for (uint32_t ox = threadIdx.x; ox < a.out_w; ox += blockDim.x) {
-        const uint32_t mx = q.flip ? a.out_w - 1 - ox : ox;
-        float fx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(mx), 0.5f), sx), 0.5f);
-        if (fx < 0.f) fx = 0.f;
-        uint32_t xlo = static_cast<uint32_t>(fx);
-        if (xlo > q.cw - 1) xlo = q.cw - 1;
-        const uint32_t xhi = xlo + 1 < q.cw ? xlo + 1 : q.cw - 1;
-        const float wx = __fsub_rn(fx, static_cast<float>(xlo));
-        const uint64_t pa = static_cast<uint64_t>(q.x0 + xlo) * 3, pb = static_cast<uint64_t>(q.x0 + xhi) * 3;
+        uint32_t xlo, wx;
+        resize_tap(q.flip ? a.out_w - 1 - ox : ox, a.out_w, q.cw, &xlo, &wx);
+        const uint64_t pa = static_cast<uint64_t>(q.x0 + xlo) * 3, pb = wx ? pa + 3 : pa;
+        const uint32_t w00 = (128 - wx) * (128 - wy), w01 = wx * (128 - wy);
+        const uint32_t w10 = (128 - wx) * wy, w11 = wx * wy;
 #pragma unroll
         for (uint32_t c = 0; c < 3; ++c) {
-            const float p00 = r0[pa + c], p01 = r0[pb + c], p10 = r1[pa + c], p11 = r1[pb + c];
-            const float top = __fadd_rn(p00, __fmul_rn(wx, __fsub_rn(p01, p00)));
-            const float bot = __fadd_rn(p10, __fmul_rn(wx, __fsub_rn(p11, p10)));
-            const float v = __fadd_rn(top, __fmul_rn(wy, __fsub_rn(bot, top)));
-            const float o = __fmul_rn(__fsub_rn(v, a.nc.mean255[c]), a.nc.inv_std255[c]);
+            const uint32_t v = w00 * r0[pa + c] + w01 * r0[pb + c] + w10 * r1[pa + c] +
+                               w11 * r1[pb + c];
+            const float o = __fmul_rn(__fsub_rn(fixed14(v), a.nc.mean255[c]), a.nc.inv_std255[c]);
             const uint64_t idx = k * 3 * plane + c * plane + static_cast<uint64_t>(oy) * a.out_w + ox;
             if constexpr (BF16)
                 static_cast<__nv_bfloat16*>(a.out)[idx] = __float2bfloat16_rn(o);
@@ -359,12 +365,6 @@ __global__ void __launch_bounds__(256) k_augment_resize(AugArgs a) {
     }
 }
 
-// K7 banded: one CTA per (sample, kRB output rows).  The source rows those
-// output rows tap (crop-window columns only, 16-byte aligned chunks) are
-// staged in shared memory once; per-column taps (xlo, xhi, wx) are tabled
-// once per CTA; each thread then emits pixel pairs of all three planes.  The
-// per-sample geometry comes from the id (cfg5) or the launch (fixed).
-constexpr uint32_t kRB = 8;
 constexpr uint32_t kMaxOutW = 512;
 
 // Per-sample prologue of K7, one thread per sample (the RNG chains -- source
@@ -389,131 +389,139 @@ __global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_
     items[k] = it;
 }
 
+// bytes [s, s+4) of the 8-byte pair {hi:lo} (s = sel & 3)
+__device__ __forceinline__ uint32_t f4e(uint32_t lo, uint32_t hi, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32.f4e %0, %1, %2, %3;" : "=r"(r) : "r"(lo), "r"(hi), "r"(sel));
+    return r;
+}
+
+__device__ __forceinline__ void st_cs_f32(float* p, float v) {
+    asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cs_u16(void* p, uint16_t v) {
+    asm volatile("st.global.cs.u16 [%0], %1;" ::"l"(p), "h"(v) : "memory");
+}
+
+// K7 banded: one CTA per (sample, kRB output rows), one thread per output
+// column, walking the band two rows at a time (the pair is one fp32x2).  The
+// taps are 32-bit read-only loads straight from the source rows, which stay
+// L1-resident while the band is in flight; each iteration prefetches the rows
+// of the pair kPrefetchAhead rows below into L1.  No shared-memory staging:
+// occupancy is not bound by the largest (512 px) source, and the A/B against
+// a staged-smem band kernel (profiles/r03_k7_ab.md) favoured the gathers.
+// Only words holding needed bytes are read: a far-edge column (wx = 0) taps
+// pixels (xlo-1, xlo) with weights (0, 128), and the third word is loaded
+// only when tap b spills into it.
+constexpr uint32_t kRB = 16;
+constexpr uint32_t kPrefetchAhead = 4;
+__device__ __forceinline__ void row_taps_g(const uint8_t* base, uint32_t off, uint32_t* rg,
+                                           uint32_t* bb) {
+    const uint32_t* p = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
+    const uint32_t w0 = __ldg(p), w1 = __ldg(p + 1);
+    const uint32_t w2 = (off & 3u) == 3u ? __ldg(p + 2) : 0u;
+    const uint32_t ta = f4e(w0, w1, off), tb = f4e(w1, w2, off);  // [Ra Ga Ba Rb] [Gb Bb - -]
+    *rg = __byte_perm(ta, tb, 0x4130);
+    *bb = __byte_perm(ta, tb, 0x0052);
+}
+
+__device__ __forceinline__ void bilerp_g(const uint8_t* base, uint32_t x3, uint32_t colw,
+                                         const uint4& r, uint32_t v[3]) {
+    uint32_t rg0, b0, rg1, b1;
+    row_taps_g(base, r.x + x3, &rg0, &b0);
+    row_taps_g(base, r.y + x3, &rg1, &b1);
+    const uint32_t w0 = colw * r.z, w1 = colw * r.w;  // two u16 lanes each, no carry
+    v[0] = __dp2a_lo(w0, rg0, __dp2a_lo(w1, rg1, 0u));
+    v[1] = __dp2a_hi(w0, rg0, __dp2a_hi(w1, rg1, 0u));
+    v[2] = __dp2a_lo(w0, b0, __dp2a_lo(w1, b1, 0u));
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 template <bool BF16>
-__global__ void __launch_bounds__(256) k_augment_resize_band(AugArgs a, const ResizeItem* items,
-                                                             uint32_t max_rows,
-                                                             uint32_t row_stride) {
-    extern __shared__ __align__(16) uint8_t rowbuf[];  // [max_rows][row_stride]
-    __shared__ float s_wx[kMaxOutW];
-    __shared__ uint16_t s_xlo[kMaxOutW], s_xhi[kMaxOutW];
-    __shared__ uint32_t s_shift[64];
-    __shared__ const uint8_t* s_src;
-    __shared__ Params s_prm;
-    __shared__ uint32_t s_W;
-    const uint32_t bands = (a.out_h + kRB - 1) / kRB;
-    const uint64_t k = blockIdx.x / bands;
-    const uint32_t oy0 = (blockIdx.x - static_cast<uint32_t>(k) * bands) * kRB;
+__global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
+                                                                  const ResizeItem* items) {
+    __shared__ uint4 s_row[kRB];  // {lo row offset, hi row offset (crop origin, + phase), 128-wy, wy}
+    __shared__ const uint8_t* s_base;  // sample start rounded down to 4 bytes
+    __shared__ Params s_q;
+    const uint64_t k = blockIdx.x;  // sample
+    const uint32_t oy0 = blockIdx.y * kRB;
     const uint32_t rows_out = a.out_h - oy0 < kRB ? a.out_h - oy0 : kRB;
     const uint32_t tid = threadIdx.x;
-    if (tid == 0) {
+    if (tid < rows_out) {
         const ResizeItem it = items[k];
-        s_src = it.src;
-        s_W = it.W;
-        s_prm = it.q;
-    }
-    __syncthreads();
-    const Params q = s_prm;
-    const uint32_t W = s_W;
-    const float sy = __fdiv_rn(static_cast<float>(q.ch), static_cast<float>(a.out_h));
-    const float sx = __fdiv_rn(static_cast<float>(q.cw), static_cast<float>(a.out_w));
-    // column taps (the oracle's exact op sequence)
-    for (uint32_t ox = tid; ox < a.out_w; ox += blockDim.x) {
-        const uint32_t mx = q.flip ? a.out_w - 1 - ox : ox;
-        float fx = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(mx), 0.5f), sx), 0.5f);
-        if (fx < 0.f) fx = 0.f;
-        uint32_t xlo = static_cast<uint32_t>(fx);
-        if (xlo > q.cw - 1) xlo = q.cw - 1;
-        s_xlo[ox] = static_cast<uint16_t>(xlo);
-        s_xhi[ox] = static_cast<uint16_t>(xlo + 1 < q.cw ? xlo + 1 : q.cw - 1);
-        s_wx[ox] = __fsub_rn(fx, static_cast<float>(xlo));
-    }
-    auto tap_y = [&](uint32_t oy, uint32_t* lo, uint32_t* hi, float* w) {
-        float fy = __fsub_rn(__fmul_rn(__fadd_rn(static_cast<float>(oy), 0.5f), sy), 0.5f);
-        if (fy < 0.f) fy = 0.f;
-        uint32_t ylo = static_cast<uint32_t>(fy);
-        if (ylo > q.ch - 1) ylo = q.ch - 1;
-        *lo = ylo;
-        *hi = ylo + 1 < q.ch ? ylo + 1 : q.ch - 1;
-        *w = __fsub_rn(fy, static_cast<float>(ylo));
-    };
-    uint32_t r_first, r_last, t0;
-    float tw;
-    tap_y(oy0, &r_first, &t0, &tw);
-    tap_y(oy0 + rows_out - 1, &t0, &r_last, &tw);
-    const uint32_t nrows = r_last - r_first + 1;  // <= max_rows (host bound)
-    // stage the tapped source rows: bytes [x0*3, (x0+cw)*3) of each, 16-B
-    // aligned; one warp per row, lanes over 16-byte chunks
-    {
-        const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-        for (uint32_t r = warp; r < nrows; r += nwarps) {
-            const uintptr_t g = reinterpret_cast<uintptr_t>(s_src) +
-                                static_cast<uint64_t>(q.y0 + r_first + r) * W * 3 + q.x0 * 3;
-            const uintptr_t a16 = g & ~static_cast<uintptr_t>(15);
-            const uint32_t need = static_cast<uint32_t>((g + 3ull * q.cw - a16 + 15) / 16);
-            if (lane == 0) s_shift[r] = static_cast<uint32_t>(g - a16);
-            uint8_t* dst = rowbuf + r * row_stride;
-            for (uint32_t c = lane; c < need; c += 32)
-                *reinterpret_cast<uint4*>(dst + 16 * c) =
-                    ld_nc_v4(reinterpret_cast<const void*>(a16 + 16 * c));
+        const uint32_t phase = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(it.src) & 3);
+        uint32_t ylo, wy;
+        resize_tap<uint32_t>(oy0 + tid, a.out_h, it.q.ch, &ylo, &wy);
+        const uint32_t yhi = wy ? ylo + 1 : ylo;
+        s_row[tid] = make_uint4(phase + ((it.q.y0 + ylo) * it.W + it.q.x0) * 3,
+                                phase + ((it.q.y0 + yhi) * it.W + it.q.x0) * 3, 128 - wy, wy);
+        if (tid == 0) {
+            s_base = it.src - phase;
+            s_q = it.q;
         }
     }
     __syncthreads();
-    // row taps of the band, once
-    __shared__ uint32_t s_y[kRB][2];
-    __shared__ float s_wy[kRB];
-    if (tid < rows_out) {
-        uint32_t ylo, yhi;
-        float wy;
-        tap_y(oy0 + tid, &ylo, &yhi, &wy);
-        s_y[tid][0] = (ylo - r_first) * row_stride + s_shift[ylo - r_first];
-        s_y[tid][1] = (yhi - r_first) * row_stride + s_shift[yhi - r_first];
-        s_wy[tid] = wy;
+    if (tid >= a.out_w) return;  // no barrier follows
+    const Params q = s_q;
+    const uint8_t* base = s_base;
+    const uint32_t ox = tid;
+    uint32_t xlo, wx;
+    resize_tap<uint32_t>(q.flip ? a.out_w - 1 - ox : ox, a.out_w, q.cw, &xlo, &wx);
+    uint32_t x3 = 3 * xlo, colw = (128 - wx) | (wx << 16);
+    if (wx == 0 && xlo > 0) {  // taps (xlo-1, xlo) weighted (0, 128): no read past xlo
+        x3 -= 3;
+        colw = 128u << 16;
     }
-    __syncthreads();
-    const uint64_t plane = static_cast<uint64_t>(a.out_h) * a.out_w;
-    const uint32_t pairs = a.out_w / 2;
     uint64_t mean2[3], inv2[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         mean2[c] = pk(__float_as_uint(a.nc.mean255[c]), __float_as_uint(a.nc.mean255[c]));
         inv2[c] = pk(__float_as_uint(a.nc.inv_std255[c]), __float_as_uint(a.nc.inv_std255[c]));
     }
-    const uint64_t big = 0x4B0000004B000000ull;  // {2^23, 2^23}
-    // thread -> one output pixel pair (column taps loaded once), rows strided
-    const uint32_t groups = blockDim.x / pairs;
-    const uint32_t g0 = tid / pairs;
-    if (g0 < groups) {
-        const uint32_t ox = 2 * (tid - g0 * pairs);
-        const uint64_t wx2 = pk(__float_as_uint(s_wx[ox]), __float_as_uint(s_wx[ox + 1]));
-        const uint32_t pa0 = 3u * s_xlo[ox], pb0 = 3u * s_xhi[ox];
-        const uint32_t pa1 = 3u * s_xlo[ox + 1], pb1 = 3u * s_xhi[ox + 1];
-        for (uint32_t rr = g0; rr < rows_out; rr += groups) {
-            const uint32_t oy = oy0 + rr;
-            const uint8_t* r0 = rowbuf + s_y[rr][0];
-            const uint8_t* r1 = rowbuf + s_y[rr][1];
-            const uint32_t wyb = __float_as_uint(s_wy[rr]);
-            const uint64_t wy2 = pk(wyb, wyb);
-            const uint64_t obase = k * 3 * plane + static_cast<uint64_t>(oy) * a.out_w + ox;
+    const uint64_t k512 = 0x4400000044000000ull;  // {512, 512}
+    using T = typename std::conditional<BF16, __nv_bfloat16, float>::type;
+    const uint64_t plane = static_cast<uint64_t>(a.out_h) * a.out_w;
+    const uint32_t ow = a.out_w;
+    T* pc[3];
+    pc[0] = static_cast<T*>(a.out) + k * 3 * plane + static_cast<uint64_t>(oy0) * ow + ox;
+    pc[1] = pc[0] + plane;
+    pc[2] = pc[1] + plane;
+    auto emit = [&](const uint32_t* v0, const uint32_t* v1, bool two) {
 #pragma unroll
-            for (uint32_t c = 0; c < 3; ++c) {
-                // 0x4B0000bb = 2^23 + bb: differences of these are exact byte
-                // differences, and (m - 2^23) is the byte itself -- the
-                // oracle's float arithmetic on packed fp32x2 lanes, no I2F
-                const uint64_t m00 = pk(0x4B000000u | r0[pa0 + c], 0x4B000000u | r0[pa1 + c]);
-                const uint64_t m01 = pk(0x4B000000u | r0[pb0 + c], 0x4B000000u | r0[pb1 + c]);
-                const uint64_t m10 = pk(0x4B000000u | r1[pa0 + c], 0x4B000000u | r1[pa1 + c]);
-                const uint64_t m11 = pk(0x4B000000u | r1[pb0 + c], 0x4B000000u | r1[pb1 + c]);
-                const uint64_t top = add2(sub2(m00, big), unfused(mul2(wx2, sub2(m01, m00)), a.zero));
-                const uint64_t bot = add2(sub2(m10, big), unfused(mul2(wx2, sub2(m11, m10)), a.zero));
-                const uint64_t v = add2(top, unfused(mul2(wy2, sub2(bot, top)), a.zero));
-                const uint64_t o = mul2(sub2(v, mean2[c]), inv2[c]);
-                const uint64_t idx = obase + c * plane;
-                if constexpr (BF16)
-                    *reinterpret_cast<uint32_t*>(static_cast<__nv_bfloat16*>(a.out) + idx) = bf16x2(o);
-                else
-                    *reinterpret_cast<uint64_t*>(static_cast<float*>(a.out) + idx) = o;
+        for (uint32_t c = 0; c < 3; ++c) {
+            const uint64_t m = pk(0x44000000u | v0[c], 0x44000000u | v1[c]);
+            const uint64_t o = mul2(sub2(sub2(m, k512), mean2[c]), inv2[c]);
+            if constexpr (BF16) {
+                const uint32_t h = bf16x2(o);
+                st_cs_u16(pc[c], static_cast<uint16_t>(h));
+                if (two) st_cs_u16(pc[c] + ow, static_cast<uint16_t>(h >> 16));
+            } else {
+                st_cs_f32(pc[c], __uint_as_float(lo32(o)));
+                if (two) st_cs_f32(pc[c] + ow, __uint_as_float(hi32(o)));
             }
+            pc[c] += 2 * ow;
         }
+    };
+    uint32_t rr = 0;
+    for (; rr + 1 < rows_out; rr += 2) {
+        uint32_t v0[3], v1[3];
+        if (rr + kPrefetchAhead < rows_out) {
+            // pull the source rows of a later row pair into L1 while this one computes
+            const uint4 f = s_row[rr + kPrefetchAhead];
+            prefetch_l1(base + f.x + x3);
+            prefetch_l1(base + f.y + x3);
+        }
+        bilerp_g(base, x3, colw, s_row[rr], v0);
+        bilerp_g(base, x3, colw, s_row[rr + 1], v1);
+        emit(v0, v1, true);
+    }
+    if (rr < rows_out) {  // odd band height
+        uint32_t v0[3];
+        bilerp_g(base, x3, colw, s_row[rr], v0);
+        emit(v0, v0, false);
     }
 }
 
@@ -580,29 +588,29 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
                 k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);
         });
     } else {
-        // banded kernel when its staged rows fit in shared memory
-        const uint32_t max_side = src.prefix ? kVarMin + kVarSpan - 1 : (height < width ? height : width);
-        const double scale = static_cast<double>(max_side) / spec.out_h;
-        const uint32_t max_rows = static_cast<uint32_t>(std::ceil(kRB * scale)) + 3;
-        const uint32_t max_w = src.prefix ? kVarMin + kVarSpan - 1 : width;
-        const uint32_t row_stride = ((3 * max_w + 15) / 16 + 1) * 16;
-        const size_t smem = static_cast<size_t>(max_rows) * row_stride;
-        if (spec.out_w % 2 == 0 && spec.out_w <= kMaxOutW && max_rows <= 64 && smem <= 160 * 1024) {
-            ensure_smem_attr(k_augment_resize_band<false>, ctx->device, smem);
-            ensure_smem_attr(k_augment_resize_band<true>, ctx->device, smem);
+        // banded gather kernel: 32-bit in-sample offsets, exact 32-bit taps,
+        // sources of at least 2 x 2 (a tap pair never leaves the sample)
+        const uint32_t max_side = src.prefix ? kVarMin + kVarSpan - 1 : std::min(height, width);
+        const uint64_t max_bytes =
+            src.prefix ? 3ull * (kVarMin + kVarSpan) * (kVarMin + kVarSpan) : 3ull * height * width;
+        const uint64_t tap_max = (2ull * std::max(spec.out_h, spec.out_w) + 1) * 64 * max_side;
+        if (spec.out_w <= kMaxOutW && tap_max < (1ull << 32) && max_bytes < (1ull << 31) &&
+            (src.prefix || std::min(height, width) >= 2)) {
+            require(n < (1ull << 31), "augment: too many samples in one launch");
             DevBuf& items = ctx->buf("resize.items", sizeof(ResizeItem) * n);
             launch(ctx, "resize_prep", [&] {
                 k_resize_prep<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(
                     a, items.as<ResizeItem>(), n);
             });
-            const dim3 grid(static_cast<unsigned>(n * ((spec.out_h + kRB - 1) / kRB)));
+            const dim3 grid(static_cast<unsigned>(n), (spec.out_h + kRB - 1) / kRB);
+            const unsigned threads = 32 * ((spec.out_w + 31) / 32);
             launch(ctx, "augment_resize", [&] {
                 if (bf16)
-                    k_augment_resize_band<true><<<grid, 256, smem, ctx->stream>>>(
-                        a, items.as<ResizeItem>(), max_rows, row_stride);
+                    k_augment_resize_rows<true><<<grid, threads, 0, ctx->stream>>>(
+                        a, items.as<ResizeItem>());
                 else
-                    k_augment_resize_band<false><<<grid, 256, smem, ctx->stream>>>(
-                        a, items.as<ResizeItem>(), max_rows, row_stride);
+                    k_augment_resize_rows<false><<<grid, threads, 0, ctx->stream>>>(
+                        a, items.as<ResizeItem>());
             });
             return;
         }

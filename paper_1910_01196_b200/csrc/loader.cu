@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -762,6 +763,14 @@ void prefetch_plan(ll_loader* ld, uint64_t next_epoch) {
     const int k = ld->cur ^ 1;
     auto& sl = ld->slot[k];
     if (sl.epoch == static_cast<int64_t>(next_epoch)) return;
+    // LL_PLAN_PREFETCH: "stream" (default) / "inline" (loader stream) / "off"
+    static const char* mode_env = std::getenv("LL_PLAN_PREFETCH");
+    const std::string mode = mode_env ? mode_env : "stream";
+    if (mode == "off") return;
+    if (mode == "inline") {
+        plan_into(ld, k, next_epoch, ctx->stream);
+        return;
+    }
     if (!ld->plan_stream) {
         // highest priority: the permutation is a cooperative launch, and its
         // blocks must win SMs back from the running augment grids promptly

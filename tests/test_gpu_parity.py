@@ -320,6 +320,19 @@ def test_resize_augment_vs_oracle(dtype):
         assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("oh,ow", [(37, 45), (5, 1), (230, 300), (96, 600), (448, 512)])
+def test_resize_augment_odd_shapes_vs_oracle(oh, ow):
+    """Banded K7 with partial warps / odd band heights / upscaling, and the
+    unbanded kernel (out_w > 512); both bit-exact vs the oracle."""
+    for sid in [5, 6]:
+        H, W = oracle.sample_hw(42, sid)
+        src = oracle.gen_sample(42, sid, H * W * 3)
+        got = device_augment(src[None], np.array([sid], np.uint64), H, W, 42, 1, mode="resize",
+                             oh=oh, ow=ow)[0]
+        want = oracle.augment(src.reshape(H, W, 3), sid, 42, 1, oh, ow, mode=oracle.AUG_RESIZE)
+        assert np.array_equal(got, want), (oh, ow, H, W)
+
+
 def test_augment_params_vs_oracle():
     import ctypes as C
     ids = np.arange(1000, dtype=np.uint64) * 7919

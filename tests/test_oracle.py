@@ -188,41 +188,39 @@ def test_aug_params_cover_range_and_flip():
 
 
 def _np_resize(src, prm, out_h, out_w):
+    """Independent numpy restatement of the fixed-point bilinear."""
     y0, x0, ch, cw, flip = prm
     m255, inv = oracle.norm_constants()
-    f = np.float32
-    sy = f(ch) / f(out_h)
-    sx = f(cw) / f(out_w)
-    out = np.empty((3, out_h, out_w), np.float32)
-    for oy in range(out_h):
-        fy = max(f(f(f(oy) + f(0.5)) * sy) - f(0.5), f(0))
-        ylo = min(int(fy), ch - 1)
-        yhi = min(ylo + 1, ch - 1)
-        wy = f(fy - f(ylo))
-        for ox in range(out_w):
-            mx = out_w - 1 - ox if flip else ox
-            fx = max(f(f(f(mx) + f(0.5)) * sx) - f(0.5), f(0))
-            xlo = min(int(fx), cw - 1)
-            xhi = min(xlo + 1, cw - 1)
-            wx = f(fx - f(xlo))
-            for c in range(3):
-                p00 = f(src[y0 + ylo, x0 + xlo, c]); p01 = f(src[y0 + ylo, x0 + xhi, c])
-                p10 = f(src[y0 + yhi, x0 + xlo, c]); p11 = f(src[y0 + yhi, x0 + xhi, c])
-                top = f(p00 + f(wx * f(p01 - p00)))
-                bot = f(p10 + f(wx * f(p11 - p10)))
-                v = f(top + f(wy * f(bot - top)))
-                out[c, oy, ox] = f(f(v - m255[c]) * inv[c])
-    return out
+
+    def taps(n_out, extent):
+        o = np.arange(n_out, dtype=np.int64)
+        f = np.maximum((2 * o + 1) * extent * 64 // n_out - 64, 0)
+        lo, w = f >> 7, f & 127
+        edge = lo >= extent - 1
+        lo[edge], w[edge] = extent - 1, 0
+        return lo, w, np.where(w > 0, lo + 1, lo)
+
+    ylo, wy, yhi = taps(out_h, ch)
+    xlo, wx, xhi = taps(out_w, cw)
+    if flip:
+        xlo, wx, xhi = xlo[::-1], wx[::-1], xhi[::-1]
+    s = src[y0:y0 + ch, x0:x0 + cw].astype(np.int64)
+    wy, wx = wy[:, None, None], wx[None, :, None]
+    v = ((128 - wy) * (128 - wx) * s[ylo][:, xlo] + (128 - wy) * wx * s[ylo][:, xhi]
+         + wy * (128 - wx) * s[yhi][:, xlo] + wy * wx * s[yhi][:, xhi])
+    assert v.max() < 2 ** 22
+    val = v.astype(np.float32) * np.float32(2.0 ** -14)
+    return ((val - m255) * inv).astype(np.float32).transpose(2, 0, 1)
 
 
 def test_resize_oracle_matches_numpy():
-    for sid in [3, 8]:
+    for sid, (oh, ow) in [(3, (24, 20)), (8, (224, 224)), (11, (300, 7)), (5, (1, 1))]:
         H, W = oracle.sample_hw(42, sid)
         assert 128 <= H <= 512 and 128 <= W <= 512
         src = oracle.gen_sample(42, sid, H * W * 3).reshape(H, W, 3)
-        prm = oracle.aug_params(42, 0, sid, H, W, 24, 20, oracle.AUG_RESIZE)
-        got = oracle.augment(src, sid, 42, 0, 24, 20, oracle.AUG_RESIZE)
-        assert np.array_equal(got, _np_resize(src, prm, 24, 20))
+        prm = oracle.aug_params(42, 0, sid, H, W, oh, ow, oracle.AUG_RESIZE)
+        got = oracle.augment(src, sid, 42, 0, oh, ow, oracle.AUG_RESIZE)
+        assert np.array_equal(got, _np_resize(src, prm, oh, ow))
 
 
 # ---- live reference cross-checks (build container / wherever oracle/_ref exists)
