@@ -166,6 +166,32 @@ int ll_augment_params(ll_ctx* ctx, const ll_augment_spec* spec, uint64_t seed, u
                       const uint64_t* host_ids, uint64_t n, uint32_t height, uint32_t width,
                       uint32_t* host_params5);
 
+/* ---- equivalence: proj/include/locload/equivalence.hpp ----------------- */
+/* Consumer side: synchronous SGD of p learners on the least-squares toy
+ * objective (per-sample loss 0.5 (w.x_i - y_i)^2), run_training
+ * (equivalence.cpp:95-174) on the device.  host_xs[n*dims] / host_ys[n] are
+ * ToyObjective::synthesize's data (equivalence.cpp:12-37).  Every step the
+ * epoch's batch goes through the scheme's assignment; aggregation CANONICAL
+ * sums per-sample gradients in ascending sample id, LEARNER_ORDER sums per
+ * learner list then across learners.  Outputs host_final_w[dims] and, if not
+ * NULL, host_step_grads[steps*dims] (each normalised by B).  Bit-identical to
+ * the reference.  Errors: p = 0, B outside [1, n], p not dividing B under the
+ * regular scheme (the reference's messages); p > 64; n >= 2^32. */
+enum { LL_AGG_CANONICAL = 0, LL_AGG_LEARNER_ORDER = 1 };
+int ll_train_run(ll_ctx* ctx, const double* host_xs, const double* host_ys, uint64_t n,
+                 uint32_t dims, int scheme, uint32_t p, uint64_t batch_size, uint64_t steps,
+                 uint64_t seed, double learning_rate, int aggregation, double* host_final_w,
+                 double* host_step_grads);
+/* ToyObjective::synthesize (equivalence.cpp:12-37), host-only: host_xs[n*dims],
+ * host_ys[n] from the seeded streams, bit-identical to the reference (same
+ * Box-Muller draws through the host libm). */
+int ll_toy_synthesize(uint64_t n, uint32_t dims, uint64_t seed, double* host_xs, double* host_ys);
+/* full_batch_gradient (equivalence.cpp:190-205): the batch's mean gradient at
+ * host_w, summed in batch-sequence order.  host_grad[dims]. */
+int ll_full_batch_gradient(ll_ctx* ctx, const double* host_xs, const double* host_ys, uint64_t n,
+                           uint32_t dims, const double* host_w, const uint64_t* host_batch,
+                           uint64_t batch_size, double* host_grad);
+
 /* ---- loader: pipeline.hpp:46-128 ---------------------------------------- */
 typedef struct ll_loader_config {
     uint64_t d;               /* DatasetSpec::n                                 */

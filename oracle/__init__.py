@@ -151,6 +151,14 @@ def ref() -> C.CDLL:
         L.ref_loader_epoch.argtypes = [C.c_char_p, C.c_uint64, C.c_uint64, C.c_uint32,
                                        C.c_uint32, C.c_uint32, C.c_uint64, C.c_int, C.c_uint64,
                                        C.c_uint64, C.POINTER(C.c_double), u64p, u64p]
+        f64p = C.POINTER(C.c_double)
+        L.ref_run_training.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_int, C.c_uint32,
+                                       C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_int,
+                                       f64p, f64p]
+        L.ref_full_batch_gradient.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, f64p, u64p,
+                                              C.c_uint64, f64p]
+        L.ref_sample_gradient.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, f64p, C.c_uint64,
+                                          f64p, f64p]
         _ref = L
     return _ref
 
@@ -389,3 +397,37 @@ def ref_gen_sample(data_seed: int, sid: int, nbytes: int, tmpdir: str) -> np.nda
     _ref_check(ref().ref_sample_path(root.encode(), sid, buf, 4096))
     with open(buf.value.decode(), "rb") as f:
         return np.frombuffer(f.read(), np.uint8)
+
+
+# ------------------------------------------------- equivalence (reference)
+_SCHEMES = {"regular": 0, "locality": 1, "locality_balanced": 2}
+
+
+def ref_run_training(n: int, dims: int, obj_seed: int, scheme: str, p: int, b: int, steps: int,
+                     seed: int, lr: float, agg: str = "canonical"):
+    """The compiled reference's run_training on ToyObjective::synthesize(n, dims,
+    obj_seed): (final_weights[dims], step_gradients[steps][dims])."""
+    w = np.empty(dims, np.float64)
+    g = np.empty((max(steps, 1), dims), np.float64)
+    _ref_check(ref().ref_run_training(n, dims, obj_seed, _SCHEMES[scheme], p, b, steps, seed, lr,
+                                      0 if agg == "canonical" else 1, _p(w, C.c_double),
+                                      _p(g, C.c_double)))
+    return w, g[:steps]
+
+
+def ref_full_batch_gradient(n: int, dims: int, obj_seed: int, w, batch) -> np.ndarray:
+    w = np.ascontiguousarray(w, np.float64)
+    b = np.ascontiguousarray(batch, np.uint64)
+    out = np.empty(dims, np.float64)
+    _ref_check(ref().ref_full_batch_gradient(n, dims, obj_seed, _p(w, C.c_double),
+                                             _p(b, C.c_uint64), len(b), _p(out, C.c_double)))
+    return out
+
+
+def ref_sample_gradient(n: int, dims: int, obj_seed: int, w, i: int):
+    w = np.ascontiguousarray(w, np.float64)
+    out = np.empty(dims, np.float64)
+    loss = C.c_double()
+    _ref_check(ref().ref_sample_gradient(n, dims, obj_seed, _p(w, C.c_double), i,
+                                         _p(out, C.c_double), C.byref(loss)))
+    return out, loss.value

@@ -19,6 +19,7 @@
 
 #include "locload/balance.hpp"
 #include "locload/core.hpp"
+#include "locload/equivalence.hpp"
 #include "locload/pipeline.hpp"
 #include "locload/rng.hpp"
 #include "locload/sampling.hpp"
@@ -264,6 +265,46 @@ int ref_loader_epoch(const char* root, uint64_t n, uint64_t sample_bytes, uint32
         *samples_per_s = r.samples_per_second;
         *hits = r.cache_hits;
         *misses = r.cache_misses;
+    });
+}
+
+// equivalence.hpp: the reference's own synthesis and training runs
+int ref_run_training(uint64_t n, uint32_t dims, uint64_t obj_seed, int scheme, uint32_t p,
+                     uint64_t b, uint64_t steps, uint64_t seed, double lr, int agg,
+                     double* final_w, double* step_grads) {
+    return guarded([&] {
+        const ToyObjective obj = ToyObjective::synthesize(n, dims, obj_seed);
+        const SchemeKind sk = scheme == 0 ? SchemeKind::regular
+                              : scheme == 1 ? SchemeKind::locality
+                                            : SchemeKind::locality_balanced;
+        const TrainingRun run = run_training(obj, sk, p, b, steps, seed, lr,
+                                             agg == 0 ? Aggregation::canonical
+                                                      : Aggregation::learner_order);
+        std::memcpy(final_w, run.final_weights.data(), sizeof(double) * dims);
+        for (uint64_t t = 0; t < steps; ++t)
+            std::memcpy(step_grads + t * dims, run.step_gradients[t].data(), sizeof(double) * dims);
+    });
+}
+int ref_full_batch_gradient(uint64_t n, uint32_t dims, uint64_t obj_seed, const double* w,
+                            const uint64_t* batch, uint64_t b, double* out) {
+    return guarded([&] {
+        const ToyObjective obj = ToyObjective::synthesize(n, dims, obj_seed);
+        GlobalBatch g;
+        g.samples.assign(batch, batch + b);
+        const std::vector<double> r =
+            full_batch_gradient(obj, std::vector<double>(w, w + dims), g);
+        std::memcpy(out, r.data(), sizeof(double) * dims);
+    });
+}
+int ref_sample_gradient(uint64_t n, uint32_t dims, uint64_t obj_seed, const double* w,
+                        uint64_t i, double* out, double* loss) {
+    return guarded([&] {
+        const ToyObjective obj = ToyObjective::synthesize(n, dims, obj_seed);
+        const std::vector<double> wv(w, w + dims);
+        std::vector<double> g;
+        obj.sample_gradient(wv, i, g);
+        std::memcpy(out, g.data(), sizeof(double) * dims);
+        *loss = obj.sample_loss(wv, i);
     });
 }
 

@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("LL_LIB", os.path.join(HERE, "liblocload_b200.so"))
 
 LL_OK, LL_ERR_INVALID, LL_ERR_RUNTIME, LL_ERR_CUDA, LL_ERR_NCCL, LL_ERR_UNSUPPORTED = range(6)
 SCHEME_REGULAR, SCHEME_LOCALITY, SCHEME_LOCALITY_BALANCED = 0, 1, 2
+AGG_CANONICAL, AGG_LEARNER_ORDER = 0, 1
 EXCHANGE_NONE, EXCHANGE_NCCL, EXCHANGE_P2P = 0, 1, 2
 OUT_F32, OUT_BF16 = 0, 1
 AUG_CROP, AUG_RESIZE = 0, 1
@@ -22,6 +23,7 @@ u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)
 u64p = C.POINTER(C.c_uint64)
 i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
 
 
 class Move(C.Structure):
@@ -92,6 +94,12 @@ PROTOTYPES = {
                                    C.POINTER(Move), u32p]),
     "ll_exchange_plan": (C.c_int, [C.POINTER(Move), C.c_uint32, u64p, C.c_uint32, C.c_uint32,
                                    C.POINTER(Xfer), u32p]),
+    "ll_train_run": (C.c_int, [C.c_void_p, f64p, f64p, C.c_uint64, C.c_uint32, C.c_int,
+                               C.c_uint32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double, C.c_int,
+                               f64p, f64p]),
+    "ll_toy_synthesize": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint64, f64p, f64p]),
+    "ll_full_batch_gradient": (C.c_int, [C.c_void_p, f64p, f64p, C.c_uint64, C.c_uint32, f64p,
+                                         u64p, C.c_uint64, f64p]),
     "ll_loader_link_peers": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32]),
     "ll_generate_samples": (C.c_int, [C.c_void_p, C.c_uint64, u64p, C.c_uint64, C.c_uint64,
                                       u8p]),

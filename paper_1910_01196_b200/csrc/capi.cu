@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "ll_internal.h"
+#include "locload/equivalence.hpp"
 
 namespace ll {
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
@@ -481,6 +482,58 @@ int ll_loader_open_peers(ll_loader* ld, const uint8_t* handles) {
 }
 int ll_loader_link_peers(ll_loader* const* loaders, uint32_t n) {
     return guarded([&] { loader_link_peers(loaders, n); });
+}
+
+// equivalence.cpp:95-174 (run_training) and :190-205 (full_batch_gradient)
+int ll_train_run(ll_ctx* ctx, const double* host_xs, const double* host_ys, uint64_t n,
+                 uint32_t dims, int scheme, uint32_t p, uint64_t batch_size, uint64_t steps,
+                 uint64_t seed, double learning_rate, int aggregation, double* host_final_w,
+                 double* host_step_grads) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(n >= 1 && dims >= 1, "ToyObjective: need n >= 1 and dims >= 1");
+        require(p != 0, "run_training: need at least one learner");
+        require(batch_size != 0 && batch_size <= n, "run_training: batch size must be in [1, n]");
+        require(scheme >= LL_SCHEME_REGULAR && scheme <= LL_SCHEME_LOCALITY_BALANCED,
+                "run_training: unknown scheme");
+        require(aggregation == LL_AGG_CANONICAL || aggregation == LL_AGG_LEARNER_ORDER,
+                "run_training: unknown aggregation");
+        if (scheme == LL_SCHEME_REGULAR)
+            require(batch_size % p == 0, "reg_slice: learner count must divide the batch size");
+        require(p <= kMaxP, "run_training: learner count must be in [1, 64] on the device");
+        require(n < 0xFFFFFFFFull, "run_training: sample count must be < 2^32 - 1");
+        require(host_xs && host_ys && host_final_w, "run_training: null buffer");
+        train_run_device(ctx, host_xs, host_ys, n, dims, scheme, p, batch_size, steps, seed,
+                         learning_rate, aggregation, host_final_w, host_step_grads);
+    });
+}
+
+// pure host logic (no device)
+int ll_toy_synthesize(uint64_t n, uint32_t dims, uint64_t seed, double* host_xs, double* host_ys) {
+    return guarded([&] {
+        require(n >= 1 && dims >= 1, "ToyObjective: need n >= 1 and dims >= 1");
+        const locload::ToyObjective obj = locload::ToyObjective::synthesize(n, dims, seed);
+        std::copy(obj.xs().begin(), obj.xs().end(), host_xs);
+        std::copy(obj.ys().begin(), obj.ys().end(), host_ys);
+    });
+}
+
+int ll_full_batch_gradient(ll_ctx* ctx, const double* host_xs, const double* host_ys, uint64_t n,
+                           uint32_t dims, const double* host_w, const uint64_t* host_batch,
+                           uint64_t batch_size, double* host_grad) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(n >= 1 && dims >= 1, "ToyObjective: need n >= 1 and dims >= 1");
+        require(n < 0xFFFFFFFFull, "full_batch_gradient: sample count must be < 2^32 - 1");
+        for (uint64_t i = 0; i < batch_size; ++i)
+            require(host_batch[i] < n, "full_batch_gradient: sample id out of range");
+        if (batch_size == 0) {  // 0 * (1.0 / 0) per coordinate, as the reference computes
+            for (uint32_t k = 0; k < dims; ++k) host_grad[k] = 0.0 * (1.0 / 0.0);
+            return;
+        }
+        full_batch_gradient_device(ctx, host_xs, host_ys, n, dims, host_w, host_batch,
+                                   batch_size, host_grad);
+    });
 }
 
 // pure host logic (no device): usable on CPU-only hosts

@@ -13,7 +13,9 @@
 
 #include "locload/balance.hpp"
 #include "locload/core.hpp"
+#include "locload/equivalence.hpp"
 #include "locload/gpu.hpp"
+#include "locload/rng.hpp"
 #include "locload/sampling.hpp"
 #include "locload_b200.h"
 
@@ -326,4 +328,90 @@ EpochReport DeviceLoader::run_epoch(std::uint64_t epoch, const DeviceBatchConsum
 }
 
 } // namespace gpu
+
+// ---- equivalence (equivalence.hpp): data on the host, training on the device
+
+ToyObjective ToyObjective::synthesize(std::uint64_t n, std::size_t dims, std::uint64_t seed) {
+    if (n == 0 || dims == 0) throw std::invalid_argument("ToyObjective: need n >= 1 and dims >= 1");
+    ToyObjective obj;
+    obj.n_ = n;
+    obj.m_ = dims;
+    obj.xs_.resize(n * dims);
+    obj.ys_.resize(n);
+    // ground truth from stream (seed, 0xfeed); sample i from (seed, i, 0x5a11):
+    // dims gaussians, then y = dot(truth, x) + 0.1 * gaussian  (equivalence.cpp:22-35)
+    std::vector<double> truth(dims);
+    SplitMix64 tr(derive_seed(seed, 0xfeedULL));
+    for (double& t : truth) t = tr.next_gaussian();
+    for (std::uint64_t i = 0; i < n; ++i) {
+        SplitMix64 r(derive_seed(seed, i, 0x5a11ULL));
+        double dot = 0;
+        double* x = &obj.xs_[i * dims];
+        for (std::size_t k = 0; k < dims; ++k) {
+            x[k] = r.next_gaussian();
+            dot += truth[k] * x[k];
+        }
+        obj.ys_[i] = dot + 0.1 * r.next_gaussian();
+    }
+    return obj;
+}
+
+double ToyObjective::sample_loss(const std::vector<double>& w, SampleId i) const {
+    const double* x = &xs_[i * m_];
+    double dot = 0;
+    for (std::size_t k = 0; k < m_; ++k) dot += w[k] * x[k];
+    const double r = dot - ys_[i];
+    return 0.5 * r * r;
+}
+
+void ToyObjective::sample_gradient(const std::vector<double>& w, SampleId i,
+                                   std::vector<double>& out) const {
+    const double* x = &xs_[i * m_];
+    double dot = 0;
+    for (std::size_t k = 0; k < m_; ++k) dot += w[k] * x[k];
+    const double r = dot - ys_[i];
+    out.resize(m_);
+    for (std::size_t k = 0; k < m_; ++k) out[k] = r * x[k];
+}
+
+TrainingRun run_training(const ToyObjective& obj, SchemeKind scheme, std::uint32_t p,
+                         std::uint64_t batch_size, std::uint64_t steps, std::uint64_t seed,
+                         double learning_rate, Aggregation agg) {
+    const int sc = scheme == SchemeKind::regular    ? LL_SCHEME_REGULAR
+                   : scheme == SchemeKind::locality ? LL_SCHEME_LOCALITY
+                                                    : LL_SCHEME_LOCALITY_BALANCED;
+    const int ag = agg == Aggregation::canonical ? LL_AGG_CANONICAL : LL_AGG_LEARNER_ORDER;
+    const std::size_t m = obj.dims();
+    TrainingRun run;
+    run.final_weights.assign(m, 0.0);
+    std::vector<double> grads(steps * m);
+    check(ll_train_run(ctx(), obj.xs().data(), obj.ys().data(), obj.samples(),
+                       static_cast<std::uint32_t>(m), sc, p, batch_size, steps, seed,
+                       learning_rate, ag, run.final_weights.data(), grads.data()));
+    run.step_gradients.resize(steps);
+    for (std::uint64_t t = 0; t < steps; ++t)
+        run.step_gradients[t].assign(grads.begin() + t * m, grads.begin() + (t + 1) * m);
+    return run;
+}
+
+std::pair<TrainingRun, TrainingRun>
+run_training_imbalanced_vs_balanced(const ToyObjective& obj, std::uint32_t p,
+                                    std::uint64_t batch_size, std::uint64_t steps,
+                                    std::uint64_t seed, double learning_rate) {
+    TrainingRun loc =
+        run_training(obj, SchemeKind::locality, p, batch_size, steps, seed, learning_rate);
+    TrainingRun bal = run_training(obj, SchemeKind::locality_balanced, p, batch_size, steps,
+                                   seed, learning_rate);
+    return {std::move(loc), std::move(bal)};
+}
+
+std::vector<double> full_batch_gradient(const ToyObjective& obj, const std::vector<double>& w,
+                                        const GlobalBatch& batch) {
+    std::vector<double> g(obj.dims());
+    check(ll_full_batch_gradient(ctx(), obj.xs().data(), obj.ys().data(), obj.samples(),
+                                 static_cast<std::uint32_t>(obj.dims()), w.data(),
+                                 batch.samples.data(), batch.samples.size(), g.data()));
+    return g;
+}
+
 } // namespace locload

@@ -123,6 +123,8 @@ void launch(ll_ctx* ctx, const char* name, F&& f) {
 }
 
 void set_device(ll_ctx* ctx);
+// capi.cu: u64 ids -> u32 on ctx->stream
+void narrow_device(ll_ctx* ctx, const uint64_t* in, uint32_t* out, uint64_t n);
 
 // permute.cu: full permutation of [0,d) into d_order (u32), on ctx->stream.
 // `tag` names the scratch buffers (independent permutations may be in flight
@@ -221,5 +223,14 @@ std::vector<ll_xfer> exchange_plan(const ll_move* moves, uint32_t n, const uint6
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
                  uint8_t* packbuf);
+
+// train.cu: consumer side (equivalence.cpp:95-205) on the device
+void train_run_device(ll_ctx* ctx, const double* h_xs, const double* h_ys, uint64_t n,
+                      uint32_t dims, int scheme, uint32_t p, uint64_t B, uint64_t steps,
+                      uint64_t seed, double lr, int aggregation, double* h_final_w,
+                      double* h_step_grads);
+void full_batch_gradient_device(ll_ctx* ctx, const double* h_xs, const double* h_ys, uint64_t n,
+                                uint32_t dims, const double* h_w, const uint64_t* h_batch,
+                                uint64_t B, double* h_grad);
 
 } // namespace ll

@@ -32,7 +32,6 @@
 
 namespace ll {
 void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
-void narrow_device(ll_ctx* ctx, const uint64_t* in, uint32_t* out, uint64_t n);
 }
 
 #define LL_NCCL(x)                                                                        \

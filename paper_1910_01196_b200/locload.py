@@ -307,3 +307,77 @@ def assign(batch: GlobalBatch, scheme: str, p: int, dir: CacheDirectory,
     a = assign_batch(batch.samples, dir.dataset_size(), p, dir.cached_fraction(),
                      SchemeKind[scheme], device)
     return [LocalAssignment(j, batch.step, lst.copy()) for j, lst in enumerate(a.lists())]
+
+
+# --------------------------------------------------------- equivalence.hpp
+class ToyObjective:
+    """equivalence.hpp:12-33: least-squares data, synthesised on the host by
+    the library (ll_toy_synthesize, bit-identical to equivalence.cpp:12-37)."""
+
+    def __init__(self, xs: np.ndarray, ys: np.ndarray):
+        self.xs = xs
+        self.ys = ys
+
+    @staticmethod
+    def synthesize(n: int, dims: int, seed: int) -> "ToyObjective":
+        if n <= 0 or dims <= 0:
+            raise InvalidArgument("ToyObjective: need n >= 1 and dims >= 1")
+        xs = np.empty(n * dims, np.float64)
+        ys = np.empty(n, np.float64)
+        check(_capi.lib().ll_toy_synthesize(n, dims, seed, ptr(xs, C.c_double),
+                                            ptr(ys, C.c_double)))
+        return ToyObjective(xs.reshape(n, dims), ys)
+
+    def samples(self) -> int:
+        return self.ys.shape[0]
+
+    def dims(self) -> int:
+        return self.xs.shape[1]
+
+
+@dataclass
+class TrainingRun:  # equivalence.hpp:52-55
+    final_weights: np.ndarray
+    step_gradients: np.ndarray  # [steps][dims], each normalised by B
+
+
+Aggregation = {"canonical": _capi.AGG_CANONICAL, "learner_order": _capi.AGG_LEARNER_ORDER}
+
+
+def run_training(obj: ToyObjective, scheme: str, p: int, batch_size: int, steps: int, seed: int,
+                 learning_rate: float, agg: str = "canonical", device: int = 0) -> TrainingRun:
+    """equivalence.cpp:95-174 on the device (ll_train_run)."""
+    if scheme not in SchemeKind:
+        raise InvalidArgument(f"run_training: unknown scheme {scheme!r}")
+    xs = np.ascontiguousarray(obj.xs, np.float64)
+    ys = np.ascontiguousarray(obj.ys, np.float64)
+    w = np.empty(obj.dims(), np.float64)
+    g = np.empty((max(steps, 1), obj.dims()), np.float64)
+    check(_capi.lib().ll_train_run(context(device), ptr(xs, C.c_double), ptr(ys, C.c_double),
+                                   obj.samples(), obj.dims(), SchemeKind[scheme], p, batch_size,
+                                   steps, seed, learning_rate, Aggregation[agg],
+                                   ptr(w, C.c_double), ptr(g, C.c_double)))
+    return TrainingRun(w, g[:steps])
+
+
+def run_training_imbalanced_vs_balanced(obj: ToyObjective, p: int, batch_size: int, steps: int,
+                                        seed: int, learning_rate: float, device: int = 0):
+    """equivalence.hpp:64-67."""
+    return (run_training(obj, "locality", p, batch_size, steps, seed, learning_rate,
+                         device=device),
+            run_training(obj, "locality_balanced", p, batch_size, steps, seed, learning_rate,
+                         device=device))
+
+
+def full_batch_gradient(obj: ToyObjective, w, batch: GlobalBatch, device: int = 0) -> np.ndarray:
+    """equivalence.cpp:190-205 on the device."""
+    xs = np.ascontiguousarray(obj.xs, np.float64)
+    ys = np.ascontiguousarray(obj.ys, np.float64)
+    w = np.ascontiguousarray(w, np.float64)
+    ids = np.ascontiguousarray(batch.samples, np.uint64)
+    out = np.empty(obj.dims(), np.float64)
+    check(_capi.lib().ll_full_batch_gradient(context(device), ptr(xs, C.c_double),
+                                             ptr(ys, C.c_double), obj.samples(), obj.dims(),
+                                             ptr(w, C.c_double), ptr(ids, C.c_uint64), len(ids),
+                                             ptr(out, C.c_double)))
+    return out

@@ -105,3 +105,26 @@ def test_exchange_plan_delivers_the_tail_moves():
 def test_exchange_plan_rejects_bad_rank():
     with pytest.raises(_capi.InvalidArgument):
         exchange_plan([], [0, 1], 1, 3)
+
+
+def test_toy_synthesize_matches_reference():
+    """ll_toy_synthesize (host-only) reproduces ToyObjective::synthesize
+    (equivalence.cpp:12-37): the reference's sample gradients and losses
+    recomputed from our data agree bit for bit."""
+    import oracle
+    from paper_1910_01196_b200 import locload as ll
+    n, dims, seed = 200, 8, 5
+    obj = ll.ToyObjective.synthesize(n, dims, seed)
+    rng = np.random.default_rng(0)
+    for i in [0, 1, 99, 199]:
+        w = rng.standard_normal(dims)
+        g, loss = oracle.ref_sample_gradient(n, dims, seed, w, i)
+        x = obj.xs[i]
+        dot = 0.0
+        for k in range(dims):
+            dot = dot + w[k] * x[k]
+        r = dot - obj.ys[i]
+        assert np.array_equal(np.array([r * x[k] for k in range(dims)]), g)
+        assert 0.5 * r * r == loss
+    with pytest.raises(ValueError, match="need n >= 1"):
+        ll.ToyObjective.synthesize(0, 8, 1)

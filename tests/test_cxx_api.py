@@ -1,7 +1,7 @@
 """The reference's own doctest suites (test_core.cpp, test_sampling.cpp,
-test_balance.cpp), compiled UNMODIFIED against include/locload/*.hpp and the
-GPU-backed liblocload_b200.so (tests/cxx/Makefile), plus the C++ device-loader
-test.  The binaries are built in the build container (the reference sources
+test_balance.cpp, test_equivalence.cpp), compiled UNMODIFIED against
+include/locload/*.hpp and the GPU-backed liblocload_b200.so
+(tests/cxx/Makefile), plus the C++ device-loader test.  The binaries are built in the build container (the reference sources
 live there) and travel to the GPU box; skipped where they were not built."""
 import os
 import subprocess
@@ -10,7 +10,7 @@ import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BIN = os.path.join(HERE, "cxx", "_bin")
-SUITES = ["test_core", "test_sampling", "test_balance", "test_gpu_api"]
+SUITES = ["test_core", "test_sampling", "test_balance", "test_equivalence", "test_gpu_api"]
 
 
 @pytest.mark.gpu
