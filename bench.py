@@ -124,9 +124,13 @@ class ClockSampler:
              0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
              0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, enabled: bool = True):
         self.samples = []
         self.ok = False
+        self.err = "disabled"
+        if not enabled:
+            self._stop = threading.Event()
+            return
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -143,7 +147,8 @@ class ClockSampler:
             try:
                 mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
                 rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((mhz, rs))
+                mem = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_MEM)
+                self.samples.append((mhz, rs, mem))
             except Exception:
                 pass
             time.sleep(0.002)
@@ -163,12 +168,14 @@ class ClockSampler:
         if not self.ok:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
         mask = 0
-        for _, r in self.samples:
+        for _, r, _m in self.samples:
             mask |= r
         reasons = sorted({n for b, n in self.NAMES.items() if mask & b})
-        mhz = [m for m, _ in self.samples]
+        mhz = [m for m, _, _m in self.samples]
+        mem = [m for _, _r, m in self.samples]
         return {"sm_mhz": float(np.median(mhz)) if mhz else None,
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(mhz),
+                "mem_mhz": [min(mem), float(np.median(mem)), max(mem)] if mem else None,
                 "source": "NVML"}
 
 
@@ -346,10 +353,12 @@ def run_ours(args):
     launches0 = C.c_uint64()
     _capi.check(lib.ll_ctx_launch_count(ctx, C.byref(launches0)))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, enabled=not os.environ.get("LL_BENCH_NO_CLOCKS")) as clk:
         barrier()
         ev0.record(stream)
+        h0 = time.perf_counter()
         samples = run_steps(start, args.steps)
+        host_enqueue_s = time.perf_counter() - h0
         ev1.record(stream)
         ev1.synchronize()
         barrier()
@@ -458,6 +467,7 @@ def run_ours(args):
                 "clocks": clk.summary(),
                 "e2e": e2e,
                 "gpu_launches": int(launches1.value - launches0.value),
+                "host_enqueue_ms_per_step": host_enqueue_s * 1e3 / args.steps,
                 "roofline": {"bound": "hbm", "kernel": aug_kernel, "achieved": achieved,
                              "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": traffic, "peak_source": peak_src,
