@@ -61,8 +61,11 @@ __device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
 }
 
 // Resolve sample k of a launch: id and source bytes.
+// *far (optional): the bytes live outside this GPU's HBM (a peer shard over
+// NVLink, or the host storage tier over PCIe).
 __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* id,
-                                        const uint8_t** src) {
+                                        const uint8_t** src, bool* far = nullptr) {
+    if (far) *far = false;
     if (m.kind == 0) {
         *id = m.ids[k];
         *src = m.base + k * m.sample_bytes;
@@ -75,6 +78,7 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
     if (s >= m.cached && m.storage) {
         // storage tier (alpha < 1): uncached samples from mapped pinned host memory
         *src = m.storage + (s - m.cached) * m.sample_bytes;
+        if (far) *far = true;
     } else if (k < kept) {
         *src = m.shard + (m.prefix ? m.prefix[s] - m.prefix[m.shard_first]
                                    : (s - m.shard_first) * m.sample_bytes);
@@ -82,6 +86,7 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
         const uint32_t o = static_cast<uint32_t>(s * m.p / m.cached);
         const uint64_t first = (static_cast<uint64_t>(o) * m.cached + m.p - 1) / m.p;
         *src = m.peers[o] + (m.prefix ? m.prefix[s] - m.prefix[first] : (s - first) * m.sample_bytes);
+        if (far) *far = true;
     } else {
         *src = m.recv + (k - kept) * m.sample_bytes;
     }
@@ -371,22 +376,59 @@ constexpr uint32_t kMaxOutW = 512;
 // geometry, crop origin, flip -- and the source resolve run once per sample
 // instead of once per band CTA).
 struct ResizeItem {
-    const uint8_t* src;
+    const uint8_t* src;   // what K7 reads (the pulled copy for far samples)
     uint32_t W;
     Params q;
+    const uint8_t* from;  // far samples: 16-byte aligned start of the rows to pull
+    uint32_t bytes16;     // ... and their length (multiple of 16), else 0
 };
 
-__global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_t n) {
+// Far samples (peer shard / host storage) are pulled into local HBM before K7:
+// K7's 4-byte tap gathers are cheap from L1/L2 but one NVLink or PCIe round
+// trip each from a far source, while the pull moves the crop window's rows in
+// coalesced 16-byte loads.  `pull` = nullptr: no far sources in this launch.
+__global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_t n,
+                              uint8_t* __restrict__ pull, uint64_t pull_stride) {
     const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (k >= n) return;
     uint64_t id;
     ResizeItem it;
-    resolve(a.src, k, &id, &it.src);
+    bool far = false;
+    resolve(a.src, k, &id, &it.src, &far);
     uint32_t H = a.H, W = a.W;
     if (a.src.prefix) var_hw(a.src.data_seed, id, &H, &W);
     it.W = W;
     it.q = aug_params(a.seed, a.epoch, id, H, W, a.out_h, a.out_w, LL_AUG_RESIZE);
+    it.from = nullptr;
+    it.bytes16 = 0;
+    if (far && pull) {
+        // the window's full rows [y0, y0 + ch), widened to 16-byte alignment
+        const uint64_t row = 3ull * W;
+        const uintptr_t start = reinterpret_cast<uintptr_t>(it.src) + it.q.y0 * row;
+        const uintptr_t end = start + it.q.ch * row;
+        const uintptr_t a16 = start & ~static_cast<uintptr_t>(15);
+        uint8_t* dst = pull + k * pull_stride;
+        it.from = reinterpret_cast<const uint8_t*>(a16);
+        it.bytes16 = static_cast<uint32_t>(((end + 15) & ~static_cast<uintptr_t>(15)) - a16);
+        it.src = dst + (start - a16) - it.q.y0 * row;  // same row indexing as the original
+    }
     items[k] = it;
+}
+
+constexpr uint32_t kPullCtas = 4;  // CTAs per sample
+
+__global__ void __launch_bounds__(256) k_resize_pull(const ResizeItem* __restrict__ items,
+                                                     uint8_t* __restrict__ pull,
+                                                     uint64_t pull_stride) {
+    const uint64_t k = blockIdx.x;
+    const uint8_t* from = items[k].from;
+    if (from == nullptr) return;
+    const uint32_t chunks = items[k].bytes16 / 16;
+    uint4* dst = reinterpret_cast<uint4*>(pull + k * pull_stride);
+    const uint4* src = reinterpret_cast<const uint4*>(from);
+    for (uint32_t c = blockIdx.y * blockDim.x + threadIdx.x; c < chunks;
+         c += kPullCtas * blockDim.x)
+        dst[c] = ld_nc_v4(src + c);
 }
 
 // bytes [s, s+4) of the 8-byte pair {hi:lo} (s = sel & 3)
@@ -598,10 +640,19 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
             (src.prefix || std::min(height, width) >= 2)) {
             require(n < (1ull << 31), "augment: too many samples in one launch");
             DevBuf& items = ctx->buf("resize.items", sizeof(ResizeItem) * n);
+            // far sources possible: peer shards (P2P) or the host storage tier
+            const bool far = src.kind == 1 && (src.peers != nullptr || src.storage != nullptr);
+            const uint64_t pull_stride = (max_bytes + 15) / 16 * 16 + 32;
+            uint8_t* pull = far ? ctx->buf("resize.pull", n * pull_stride).as<uint8_t>() : nullptr;
             launch(ctx, "resize_prep", [&] {
                 k_resize_prep<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(
-                    a, items.as<ResizeItem>(), n);
+                    a, items.as<ResizeItem>(), n, pull, pull_stride);
             });
+            if (far)
+                launch(ctx, "resize_pull", [&] {
+                    k_resize_pull<<<dim3(static_cast<unsigned>(n), kPullCtas), 256, 0,
+                                    ctx->stream>>>(items.as<ResizeItem>(), pull, pull_stride);
+                });
             const dim3 grid(static_cast<unsigned>(n), (spec.out_h + kRB - 1) / kRB);
             const unsigned threads = 32 * ((spec.out_w + 31) / 32);
             launch(ctx, "augment_resize", [&] {

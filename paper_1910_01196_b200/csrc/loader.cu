@@ -754,6 +754,17 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     ld->plan_epoch = static_cast<int64_t>(epoch);
 }
 
+// The side stream carries the prefetched exchange (K5 pack + NCCL) and the
+// host-driven prologue (H2D + single-step K4).  Highest priority: its small
+// grids are scheduled ahead of the pending CTAs of the running augment grid,
+// so they complete under that augment instead of after it.
+void ensure_side_stream(ll_loader* ld) {
+    if (ld->side) return;
+    int lo = 0, hi = 0;
+    LL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    LL_CUDA(cudaStreamCreateWithPriority(&ld->side, cudaStreamNonBlocking, hi));
+}
+
 // Start planning epoch + 1 into the other slot on plan_stream, after
 // everything already issued on the loader stream (which includes every step
 // that read that slot's previous plan).
@@ -805,7 +816,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
                 LL_CUDA(cudaEventCreateWithFlags(&ld->xdone[i], cudaEventDisableTiming));
                 LL_CUDA(cudaEventCreateWithFlags(&ld->augdone[i], cudaEventDisableTiming));
             }
-            if (!ld->side) LL_CUDA(cudaStreamCreateWithFlags(&ld->side, cudaStreamNonBlocking));
+            ensure_side_stream(ld);
         }
         auto& pend = ld->xpending[slot];
         if (pend.valid && pend.epoch == epoch && pend.step == step) {
@@ -872,7 +883,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             h.stage.reserve(sizeof(ll_loader::Tables) + sizeof(uint64_t) * B);
             h.plan.reserve(1, B);
         }
-        LL_CUDA(cudaStreamCreateWithFlags(&ld->side, cudaStreamNonBlocking));
+        ensure_side_stream(ld);
     }
     auto& h = *ld->hslots[ld->submitted % F];
     h.info = ll_step_info{};

@@ -556,6 +556,39 @@ def test_loader_storage_tier_vs_oracle(p, alpha):
                 assert np.array_equal(got[k], want), (t, j, k, int(sid) >= cached)
 
 
+def test_loader_resize_far_sources_vs_oracle():
+    """K7 with far sources: a peer's shard (P2P) and the host storage tier
+    (alpha < 1) are pulled into local HBM before the tap gathers; every
+    delivered sample equals the oracle (fixed 256 x 256 sources, resize to
+    160 x 192)."""
+    d, p, B, seed, alpha = 3000, 2, 120, 42, 0.5
+    aug = AugmentConfig(mode="resize", out_h=160, out_w=192)
+    lds = []
+    for j in range(p):
+        ld = DeviceLoader(LoaderConfig(d=d, learners=p, rank=j, batch_size=B, alpha=alpha,
+                                       seed=seed, data_seed=seed, exchange="p2p", augment=aug))
+        ld.populate()
+        lds.append(ld)
+    DeviceLoader.link_peers(lds)
+    cached = oracle.cached_count(d, alpha)
+    order = oracle.permute_epoch(seed, 1, d)
+    far = 0
+    for t in [0, 7]:
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, cached, oracle.MODE_LOCALITY_BALANCED)
+        for j, ld in enumerate(lds):
+            info = ld.step(1, t)
+            lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            got = ld.fetch(info)
+            src = oracle.gen_samples(seed, lst, 256 * 256 * 3)
+            for k, sid in enumerate(lst):
+                far += int(int(sid) >= cached or k >= info.kept)
+                want = oracle.augment(src[k].reshape(256, 256, 3), int(sid), seed, 1, 160, 192,
+                                      mode=oracle.AUG_RESIZE)
+                assert np.array_equal(got[k], want), (t, j, k)
+    assert far > 0
+
+
 def test_loader_populate_from_reference_files(tmp_path):
     """Cache population from a dataset written by the REFERENCE's
     generate_dataset (oracle/_ref): the learner serves exactly the oracle's
