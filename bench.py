@@ -395,7 +395,7 @@ def run_ours(args):
     barrier()
     _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     stats = {}
-    for name in [aug_kernel, "permute", "assign", "pack"]:
+    for name in [aug_kernel, "permute", "assign", "pack", "resize_prep", "resize_pull"]:
         cnt, tot = C.c_uint64(), C.c_double()
         _capi.check(lib.ll_ctx_kernel_stats(ctx, name.encode(), C.byref(cnt), C.byref(tot)))
         stats[name] = (cnt.value, tot.value)
@@ -476,6 +476,10 @@ def run_ours(args):
                          "cache of 4096 samples"}
 
     totals = ld.epoch_totals()
+    if os.environ.get("LL_BENCH_RANK_STATS"):  # per-rank kernel times on stderr
+        print(json.dumps({"rank": rank, "kernel_ms": {k: (v[1] / v[0] if v[0] else None)
+                                                      for k, v in stats.items()}}),
+              file=sys.stderr, flush=True)
     storage = None
     if totals["uncached"] and aug_n:
         # alpha < 1: the dominant kernel also reads the uncached samples' windows

@@ -244,11 +244,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
     __shared__ const uint8_t* s_src;
     __shared__ Params s_prm;
+    __shared__ uint64_t s_k;
 
-    const uint64_t k = blockIdx.x / kBands;
-    const uint32_t band = blockIdx.x - static_cast<uint32_t>(k) * kBands;
+    const uint64_t kb = blockIdx.x / kBands;
+    const uint32_t band = blockIdx.x - static_cast<uint32_t>(kb) * kBands;
     const uint32_t tid = threadIdx.x;
     if (tid == 0) {
+        // received samples (list tail [kept, n): peer HBM over NVLink) are
+        // scheduled first, so their longer reads overlap the local ones
+        // instead of forming the grid's tail; the output slot stays k
+        uint64_t k = kb;
+        if (a.src.kind == 1) {
+            const uint64_t kept = a.src.kept_dev ? *a.src.kept_dev : a.src.kept;
+            const uint64_t nr = kept < a.n ? a.n - kept : 0;
+            k = kb < nr ? kept + kb : kb - nr;
+        }
+        s_k = k;
         uint64_t id;
         const uint8_t* src;
         resolve(a.src, k, &id, &src);
@@ -264,6 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     __syncthreads();
     const Params q = s_prm;
     const uint8_t* src = s_src;
+    const uint64_t k = s_k;
     const uint32_t row_bytes = a.W * 3;
     const uint32_t a0 = (3 * q.x0) & ~15u;
     const uint32_t nch = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
@@ -377,7 +389,7 @@ constexpr uint32_t kMaxOutW = 512;
 // instead of once per band CTA).
 struct ResizeItem {
     const uint8_t* src;   // what K7 reads (the pulled copy for far samples)
-    uint32_t W;
+    uint32_t pitch;       // row pitch in bytes: var_pitch(W) (variable), 3W (fixed)
     Params q;
     const uint8_t* from;  // far samples: 16-byte aligned start of the rows to pull
     uint32_t bytes16;     // ... and their length (multiple of 16), else 0
@@ -397,13 +409,13 @@ __global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_
     resolve(a.src, k, &id, &it.src, &far);
     uint32_t H = a.H, W = a.W;
     if (a.src.prefix) var_hw(a.src.data_seed, id, &H, &W);
-    it.W = W;
+    it.pitch = a.src.prefix ? var_pitch(W) : 3 * W;
     it.q = aug_params(a.seed, a.epoch, id, H, W, a.out_h, a.out_w, LL_AUG_RESIZE);
     it.from = nullptr;
     it.bytes16 = 0;
     if (far && pull) {
         // the window's full rows [y0, y0 + ch), widened to 16-byte alignment
-        const uint64_t row = 3ull * W;
+        const uint64_t row = it.pitch;
         const uintptr_t start = reinterpret_cast<uintptr_t>(it.src) + it.q.y0 * row;
         const uintptr_t end = start + it.q.ch * row;
         const uintptr_t a16 = start & ~static_cast<uintptr_t>(15);
@@ -478,15 +490,47 @@ __device__ __forceinline__ void bilerp_g(const uint8_t* base, uint32_t x3, uint3
     v[2] = __dp2a_lo(w0, b0, __dp2a_lo(w1, b1, 0u));
 }
 
+// Word-aligned rows (variable geometry, var_pitch): `p` = the 4-byte aligned
+// word holding tap a's first byte, `sel` = its byte phase, both per-column
+// constants.  The third word is read unconditionally (its bytes only matter
+// when sel = 3); shards and pull slots carry 16 bytes of tail slack for it.
+__device__ __forceinline__ void row_taps_a(const uint8_t* p, uint32_t sel, uint32_t* rg,
+                                           uint32_t* bb) {
+    const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+    const uint32_t w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2);
+    const uint32_t ta = f4e(w0, w1, sel), tb = f4e(w1, w2, sel);  // [Ra Ga Ba Rb] [Gb Bb - -]
+    *rg = __byte_perm(ta, tb, 0x4130);
+    *bb = __byte_perm(ta, tb, 0x0052);
+}
+
+__device__ __forceinline__ void bilerp_a(const uint8_t* colp, uint32_t sel, uint32_t colw,
+                                         const uint4& r, uint32_t v[3]) {
+    uint32_t rg0, b0, rg1, b1;
+    row_taps_a(colp + r.x, sel, &rg0, &b0);
+    row_taps_a(colp + r.y, sel, &rg1, &b1);
+    const uint32_t w0 = colw * r.z, w1 = colw * r.w;  // two u16 lanes each, no carry
+    v[0] = __dp2a_lo(w0, rg0, __dp2a_lo(w1, rg1, 0u));
+    v[1] = __dp2a_hi(w0, rg0, __dp2a_hi(w1, rg1, 0u));
+    v[2] = __dp2a_lo(w0, b0, __dp2a_lo(w1, b1, 0u));
+}
+
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
-template <bool BF16>
+// ALIGNED (word-aligned rows and sample starts): the row table holds the row
+// starts and each column keeps one pointer and byte phase, so a tap costs one
+// 64-bit add, three loads and four byte permutes.
+// OUT = 224 fixes the output geometry at compile time (cfg5), so all six
+// stores of a row pair address off one pointer with immediate offsets.
+template <bool BF16, bool ALIGNED, uint32_t OUT = 0>
 __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
                                                                   const ResizeItem* items) {
-    __shared__ uint4 s_row[kRB];  // {lo row offset, hi row offset (crop origin, + phase), 128-wy, wy}
-    __shared__ const uint8_t* s_base;  // sample start rounded down to 4 bytes
+    // {lo row offset, hi row offset, 128-wy, wy}; offsets from s_base, which is
+    // the sample start (ALIGNED) or the sample start rounded down to 4 bytes
+    // with the crop origin and the phase folded into the offsets
+    __shared__ uint4 s_row[kRB];
+    __shared__ const uint8_t* s_base;
     __shared__ Params s_q;
     const uint64_t k = blockIdx.x;  // sample
     const uint32_t oy0 = blockIdx.y * kRB;
@@ -498,10 +542,15 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
         uint32_t ylo, wy;
         resize_tap<uint32_t>(oy0 + tid, a.out_h, it.q.ch, &ylo, &wy);
         const uint32_t yhi = wy ? ylo + 1 : ylo;
-        s_row[tid] = make_uint4(phase + ((it.q.y0 + ylo) * it.W + it.q.x0) * 3,
-                                phase + ((it.q.y0 + yhi) * it.W + it.q.x0) * 3, 128 - wy, wy);
+        if (ALIGNED)
+            s_row[tid] = make_uint4((it.q.y0 + ylo) * it.pitch, (it.q.y0 + yhi) * it.pitch,
+                                    128 - wy, wy);
+        else
+            s_row[tid] = make_uint4(phase + (it.q.y0 + ylo) * it.pitch + it.q.x0 * 3,
+                                    phase + (it.q.y0 + yhi) * it.pitch + it.q.x0 * 3, 128 - wy,
+                                    wy);
         if (tid == 0) {
-            s_base = it.src - phase;
+            s_base = it.src - phase;  // phase = 0 when ALIGNED
             s_q = it.q;
         }
     }
@@ -517,6 +566,10 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
         x3 -= 3;
         colw = 128u << 16;
     }
+    // ALIGNED: this column's tap-a word in row 0 and its byte phase
+    const uint32_t xb = 3 * q.x0 + x3;
+    const uint8_t* colp = base + (xb & ~3u);
+    const uint32_t sel = xb & 3u;
     uint64_t mean2[3], inv2[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
@@ -525,8 +578,14 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
     }
     const uint64_t k512 = 0x4400000044000000ull;  // {512, 512}
     using T = typename std::conditional<BF16, __nv_bfloat16, float>::type;
-    const uint64_t plane = static_cast<uint64_t>(a.out_h) * a.out_w;
-    const uint32_t ow = a.out_w;
+    const uint32_t ow = OUT ? OUT : a.out_w;
+    const uint64_t plane = static_cast<uint64_t>(OUT ? OUT : a.out_h) * ow;
+    auto bilerp = [&](const uint4& r, uint32_t v[3]) {
+        if constexpr (ALIGNED)
+            bilerp_a(colp, sel, colw, r, v);
+        else
+            bilerp_g(base, x3, colw, r, v);
+    };
     T* pc[3];
     pc[0] = static_cast<T*>(a.out) + k * 3 * plane + static_cast<uint64_t>(oy0) * ow + ox;
     pc[1] = pc[0] + plane;
@@ -536,16 +595,18 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
         for (uint32_t c = 0; c < 3; ++c) {
             const uint64_t m = pk(0x44000000u | v0[c], 0x44000000u | v1[c]);
             const uint64_t o = mul2(sub2(sub2(m, k512), mean2[c]), inv2[c]);
+            T* pt = OUT ? pc[0] + c * plane : pc[c];
             if constexpr (BF16) {
                 const uint32_t h = bf16x2(o);
-                st_cs_u16(pc[c], static_cast<uint16_t>(h));
-                if (two) st_cs_u16(pc[c] + ow, static_cast<uint16_t>(h >> 16));
+                st_cs_u16(pt, static_cast<uint16_t>(h));
+                if (two) st_cs_u16(pt + ow, static_cast<uint16_t>(h >> 16));
             } else {
-                st_cs_f32(pc[c], __uint_as_float(lo32(o)));
-                if (two) st_cs_f32(pc[c] + ow, __uint_as_float(hi32(o)));
+                st_cs_f32(pt, __uint_as_float(lo32(o)));
+                if (two) st_cs_f32(pt + ow, __uint_as_float(hi32(o)));
             }
-            pc[c] += 2 * ow;
+            if (!OUT) pc[c] += 2 * ow;
         }
+        if (OUT) pc[0] += 2 * ow;
     };
     uint32_t rr = 0;
     for (; rr + 1 < rows_out; rr += 2) {
@@ -553,16 +614,16 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
         if (rr + kPrefetchAhead < rows_out) {
             // pull the source rows of a later row pair into L1 while this one computes
             const uint4 f = s_row[rr + kPrefetchAhead];
-            prefetch_l1(base + f.x + x3);
-            prefetch_l1(base + f.y + x3);
+            prefetch_l1((ALIGNED ? colp : base + x3) + f.x);
+            prefetch_l1((ALIGNED ? colp : base + x3) + f.y);
         }
-        bilerp_g(base, x3, colw, s_row[rr], v0);
-        bilerp_g(base, x3, colw, s_row[rr + 1], v1);
+        bilerp(s_row[rr], v0);
+        bilerp(s_row[rr + 1], v1);
         emit(v0, v1, true);
     }
     if (rr < rows_out) {  // odd band height
         uint32_t v0[3];
-        bilerp_g(base, x3, colw, s_row[rr], v0);
+        bilerp(s_row[rr], v0);
         emit(v0, v0, false);
     }
 }
@@ -655,13 +716,23 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
                 });
             const dim3 grid(static_cast<unsigned>(n), (spec.out_h + kRB - 1) / kRB);
             const unsigned threads = 32 * ((spec.out_w + 31) / 32);
+            // word-aligned rows: the variable-geometry shard layout (geometry.cuh)
+            const bool aligned = src.prefix != nullptr;
             launch(ctx, "augment_resize", [&] {
-                if (bf16)
-                    k_augment_resize_rows<true><<<grid, threads, 0, ctx->stream>>>(
-                        a, items.as<ResizeItem>());
+                const ResizeItem* it = items.as<ResizeItem>();
+                const bool out224 = spec.out_h == 224 && spec.out_w == 224;
+                if (bf16 && aligned && out224)
+                    k_augment_resize_rows<true, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
+                else if (!bf16 && aligned && out224)
+                    k_augment_resize_rows<false, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
+                else if (bf16 && aligned)
+                    k_augment_resize_rows<true, true><<<grid, threads, 0, ctx->stream>>>(a, it);
+                else if (bf16)
+                    k_augment_resize_rows<true, false><<<grid, threads, 0, ctx->stream>>>(a, it);
+                else if (aligned)
+                    k_augment_resize_rows<false, true><<<grid, threads, 0, ctx->stream>>>(a, it);
                 else
-                    k_augment_resize_rows<false><<<grid, threads, 0, ctx->stream>>>(
-                        a, items.as<ResizeItem>());
+                    k_augment_resize_rows<false, false><<<grid, threads, 0, ctx->stream>>>(a, it);
             });
             return;
         }

@@ -1,9 +1,11 @@
 // geometry.cuh -- per-sample source geometry of the variable-size dataset
 // (BASELINE configs[4], cfg5): sample id is H x W x 3 u8 HWC with
 // H, W = 128 + bounded(385) drawn from SplitMix64(derive_seed(data_seed, id, 1))
-// (oracle: lo_sample_hw).  Samples are stored back to back, each padded to 16
-// bytes; every learner computes the same global prefix of padded sizes, so a
-// sample's offset inside its owner's shard is prefix[s] - prefix[first(owner)].
+// (oracle: lo_sample_hw).  In HBM each row is padded to a 4-byte pitch
+// (var_pitch) and each sample to 16 bytes, so every row starts word aligned and
+// a bilinear tap's byte phase is a per-column constant (augment.cu K7); every
+// learner computes the same global prefix of padded sizes, so a sample's
+// offset inside its owner's shard is prefix[s] - prefix[first(owner)].
 #pragma once
 #include <cstdint>
 
@@ -21,5 +23,11 @@ LL_HD void var_hw(uint64_t data_seed, uint64_t id, uint32_t* h, uint32_t* w) {
 }
 
 LL_HD uint64_t pad16(uint64_t b) { return (b + 15) & ~15ull; }
+
+// HBM row pitch of a W-pixel u8 RGB row, and the padded bytes of an H x W sample
+LL_HD uint32_t var_pitch(uint32_t w) { return (3u * w + 3u) & ~3u; }
+LL_HD uint64_t var_bytes(uint32_t h, uint32_t w) {
+    return pad16(static_cast<uint64_t>(h) * var_pitch(w));
+}
 
 } // namespace ll

@@ -435,7 +435,8 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
         ld->h_prefix_ends.assign(ends, ends + 2);
         shard_bytes = ends[1] - ends[0];
     }
-    ld->shard.reserve(std::max<uint64_t>(shard_bytes, 16));
+    // + 16: K7's word-aligned taps read up to 8 bytes past a row's last pixel
+    ld->shard.reserve(std::max<uint64_t>(shard_bytes, 16) + 16);
     for (auto& sl : ld->slot) {
         sl.order.reserve(sizeof(uint32_t) * c.d);
         sl.plan.reserve(ld->steps, c.batch_size);
@@ -559,6 +560,21 @@ void populate_storage(ll_loader* ld) {
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+void ensure_plan_stream(ll_loader* ld);
+
+// Steady state from the first step on: the output ring, the plan stream and
+// the second plan slot (device scratch, pinned host tables) are created here,
+// not on the step path, where an allocation would synchronise the device.
+// Slot 1 is left holding epoch 1's plan, which the mid-epoch prefetch reuses.
+void prime(ll_loader* ld) {
+    ensure_out(ld);
+    ensure_plan_stream(ld);
+    if (ld->slot[1].epoch < 0) {
+        plan_into(ld, 1, 1, ld->plan_stream);
+        LL_CUDA(cudaStreamSynchronize(ld->plan_stream));
+    }
+}
+
 void loader_populate(ll_loader* ld) {
     set_device(ld->ctx);
     populate_storage(ld);
@@ -569,6 +585,7 @@ void loader_populate(ll_loader* ld) {
         generate_range_device(ld->ctx, ld->shard.as<uint8_t>(), ld->first, ld->owned, ld->S,
                           ld->cfg.data_seed);
     LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));
+    prime(ld);
     ld->populated = true;
 }
 
@@ -580,6 +597,7 @@ void loader_populate_from_host(ll_loader* ld, const uint8_t* host) {
     LL_CUDA(cudaMemcpyAsync(ld->shard.ptr, host, ld->owned * ld->S, cudaMemcpyHostToDevice,
                             ld->ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ld->ctx->stream));
+    prime(ld);
     ld->populated = true;
 }
 
@@ -605,13 +623,16 @@ uint64_t sample_size(const ll_loader* ld, uint64_t id) {
 }
 
 // Reads ids [lo, hi) into dst (host) at offsets off(id); parallel over files.
+// Variable geometry: the flat file rows land at the HBM row pitch (var_pitch).
 template <typename Off>
 void read_files(const ll_loader* ld, const std::string& root, uint64_t lo, uint64_t hi,
                 uint8_t* dst, Off off, uint32_t threads) {
     std::atomic<uint64_t> next{lo};
     std::mutex err_mu;
     std::string err;
+    const bool pitched = ld->cfg.geometry == LL_GEOM_VARIABLE;
     auto work = [&] {
+        std::vector<uint8_t> flat;
         for (;;) {
             const uint64_t id = next.fetch_add(1);
             if (id >= hi) return;
@@ -622,11 +643,24 @@ void read_files(const ll_loader* ld, const std::string& root, uint64_t lo, uint6
             if (!f) {
                 e = "sample " + std::to_string(id) + ": cannot open " + path;
             } else {
-                const size_t got = std::fread(dst + off(id), 1, want, f);
+                if (pitched) flat.resize(want);
+                uint8_t* to = pitched ? flat.data() : dst + off(id);
+                const size_t got = std::fread(to, 1, want, f);
                 std::fclose(f);
-                if (got != want)
+                if (got != want) {
                     e = "sample " + std::to_string(id) + ": truncated file " + path + " (read " +
                         std::to_string(got) + " of " + std::to_string(want) + " bytes)";
+                } else if (pitched) {
+                    uint32_t h, w;
+                    var_hw(ld->cfg.data_seed, id, &h, &w);
+                    const uint32_t row = 3 * w, pitch = var_pitch(w);
+                    uint8_t* out = dst + off(id);
+                    for (uint32_t y = 0; y < h; ++y) {
+                        std::memcpy(out + static_cast<uint64_t>(y) * pitch,
+                                    flat.data() + static_cast<uint64_t>(y) * row, row);
+                        std::memset(out + static_cast<uint64_t>(y) * pitch + row, 0, pitch - row);
+                    }
+                }
             }
             if (!e.empty()) {
                 std::lock_guard<std::mutex> g(err_mu);
@@ -714,6 +748,7 @@ void loader_populate_from_files(ll_loader* ld, const char* root_c, uint32_t thre
         read_files(ld, root, ld->cached, c.d, ld->storage,
                    [&](uint64_t s) { return (s - ld->cached) * ld->S; }, threads);
     }
+    prime(ld);
     ld->populated = true;
 }
 
@@ -765,6 +800,15 @@ void ensure_side_stream(ll_loader* ld) {
     LL_CUDA(cudaStreamCreateWithPriority(&ld->side, cudaStreamNonBlocking, hi));
 }
 
+void ensure_plan_stream(ll_loader* ld) {
+    if (ld->plan_stream) return;
+    // highest priority: the permutation is a cooperative launch, and its
+    // blocks must win SMs back from the running augment grids promptly
+    int lo = 0, hi = 0;
+    LL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    LL_CUDA(cudaStreamCreateWithPriority(&ld->plan_stream, cudaStreamNonBlocking, hi));
+}
+
 // Start planning epoch + 1 into the other slot on plan_stream, after
 // everything already issued on the loader stream (which includes every step
 // that read that slot's previous plan).
@@ -781,13 +825,7 @@ void prefetch_plan(ll_loader* ld, uint64_t next_epoch) {
         plan_into(ld, k, next_epoch, ctx->stream);
         return;
     }
-    if (!ld->plan_stream) {
-        // highest priority: the permutation is a cooperative launch, and its
-        // blocks must win SMs back from the running augment grids promptly
-        int lo = 0, hi = 0;
-        LL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        LL_CUDA(cudaStreamCreateWithPriority(&ld->plan_stream, cudaStreamNonBlocking, hi));
-    }
+    ensure_plan_stream(ld);
     cudaEvent_t issued = ctx->take_event();
     LL_CUDA(cudaEventRecord(issued, ctx->stream));
     LL_CUDA(cudaStreamWaitEvent(ld->plan_stream, issued, 0));
@@ -895,13 +933,32 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     // last used it has finished on the main stream
     cudaStream_t main = ctx->stream;
     if (h.used) LL_CUDA(cudaStreamWaitEvent(ld->side, h.done, 0));
+    const PlanDev pd = h.plan.view();
+    const bool devplan = (c.scheme == LL_SCHEME_LOCALITY_BALANCED ||
+                          c.scheme == LL_SCHEME_REGULAR) &&
+                         (p == 1 || c.exchange == LL_EXCHANGE_P2P);
+    h.synchronous = !devplan;
+    const size_t tab = sizeof(ll_loader::Tables);
+    // devplan: n_local is the balanced target / regular slice, known up front
+    if (devplan) h.n_local = B / p + (me < B % p ? 1 : 0);
     ctx->stream = ld->side;
     try {
         LL_CUDA(cudaMemcpyAsync(h.batch64.ptr, h.pin_batch, sizeof(uint64_t) * B,
                                 cudaMemcpyHostToDevice, ctx->stream));
         narrow_device(ctx, h.batch64.as<uint64_t>(), h.order.as<uint32_t>(), B);
-        assign_device(ctx, h.order.as<uint32_t>(), 1, B, p, ld->cached, c.scheme, h.plan.view(),
+        assign_device(ctx, h.order.as<uint32_t>(), 1, B, p, ld->cached, c.scheme, pd,
                       aug_plan(ld, epoch));
+        if (devplan) {
+            // the step's tables and local ids back to the host, also under the
+            // previous step's augment (they depend on the plan only)
+            launch(ctx, "stage", [&] {
+                k_stage<<<static_cast<unsigned>(
+                              std::min<uint64_t>((h.n_local + 255) / 256 + 1, 1184)),
+                          256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), h.n_local);
+            });
+            LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab + sizeof(uint64_t) * h.n_local,
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
         LL_CUDA(cudaEventRecord(h.pro_done, ctx->stream));
     } catch (...) {
         ctx->stream = main;
@@ -911,23 +968,10 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     LL_CUDA(cudaStreamWaitEvent(main, h.pro_done, 0));
     h.used = true;
     h.info.h2d_bytes = sizeof(uint64_t) * B;
-    const PlanDev pd = h.plan.view();
-    const bool devplan = (c.scheme == LL_SCHEME_LOCALITY_BALANCED ||
-                          c.scheme == LL_SCHEME_REGULAR) &&
-                         (p == 1 || c.exchange == LL_EXCHANGE_P2P);
-    h.synchronous = !devplan;
-    const size_t tab = sizeof(ll_loader::Tables);
     if (devplan) {
         // fully asynchronous: the kernel reads the list offset and kept count
-        // from the device plan; n_local is the balanced target / regular slice
-        h.n_local = B / p + (me < B % p ? 1 : 0);
+        // from the device plan
         void* out = run_step_devplan(ld, epoch, pd, h.n_local);
-        launch(ctx, "stage", [&] {
-            k_stage<<<static_cast<unsigned>(std::min<uint64_t>((h.n_local + 255) / 256 + 1, 1184)),
-                      256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), h.n_local);
-        });
-        LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab + sizeof(uint64_t) * h.n_local,
-                                cudaMemcpyDeviceToHost, ctx->stream));
         h.info.d2h_bytes = tab + sizeof(uint64_t) * h.n_local;
         h.info.device_out = reinterpret_cast<uintptr_t>(out);
     } else {

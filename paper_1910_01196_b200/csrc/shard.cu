@@ -70,7 +70,7 @@ __global__ void k_var_sizes(uint64_t* __restrict__ vals, uint64_t d, uint64_t da
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         uint32_t h, w;
         var_hw(data_seed, i, &h, &w);
-        vals[i] = pad16(3ull * h * w);
+        vals[i] = var_bytes(h, w);
     }
 }
 
@@ -100,18 +100,34 @@ __global__ void __launch_bounds__(1024) k_scan1(uint64_t* vals, uint64_t n) {
 }
 
 // One CTA per owned sample: the generate_dataset bytes of sample first+t at
-// shard + prefix[first+t] - prefix[first].
+// shard + prefix[first+t] - prefix[first], row y at y * var_pitch(w) (the
+// pitch padding is zero).  Thread per 32-bit word of the pitched rows; a word
+// spans at most two draws of the byte stream.
 __global__ void __launch_bounds__(256) k_generate_var(uint8_t* __restrict__ shard, uint64_t first,
                                                       const uint64_t* __restrict__ prefix,
                                                       uint64_t data_seed) {
     const uint64_t id = first + blockIdx.x;
     uint32_t h, w;
     var_hw(data_seed, id, &h, &w);
-    const uint64_t bytes = 3ull * h * w;
-    uint8_t* dst = shard + (prefix[id] - prefix[first]);
+    const uint32_t row = 3 * w, words = var_pitch(w) / 4;
+    uint32_t* dst = reinterpret_cast<uint32_t*>(shard + (prefix[id] - prefix[first]));
     const uint64_t key = derive_seed(data_seed, id);
-    for (uint64_t c = threadIdx.x; c < (bytes + 15) / 16; c += blockDim.x)
-        gen_chunk(dst, key, c, bytes, true);
+    for (uint32_t t = threadIdx.x; t < h * words; t += blockDim.x) {
+        const uint32_t y = t / words, q = t - y * words;
+        const uint32_t col = 4 * q;
+        uint32_t v = 0;
+        if (col < row) {
+            const uint64_t b0 = static_cast<uint64_t>(y) * row + col;  // flat byte index
+            const uint32_t sh = 8 * static_cast<uint32_t>(b0 & 7);
+            const uint64_t lo = draw_at(key, b0 >> 3);
+            uint64_t x = lo >> sh;
+            if (sh > 32) x |= draw_at(key, (b0 >> 3) + 1) << (64 - sh);
+            v = static_cast<uint32_t>(x);
+            const uint32_t valid = row - col;  // bytes of this word inside the row
+            if (valid < 4) v &= (1u << (8 * valid)) - 1;
+        }
+        dst[t] = v;
+    }
 }
 
 } // namespace
