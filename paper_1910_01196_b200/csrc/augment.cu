@@ -26,6 +26,7 @@
 #include <cmath>
 #include <type_traits>
 #include <cstdlib>
+#include <string>
 
 namespace ll {
 namespace {
@@ -392,6 +393,7 @@ struct ResizeItem {
     uint32_t pitch;       // row pitch in bytes: var_pitch(W) (variable), 3W (fixed)
     Params q;
     const uint8_t* from;  // far samples: 16-byte aligned start of the rows to pull
+    uint8_t* to;          // ... their pull slot in local HBM
     uint32_t bytes16;     // ... and their length (multiple of 16), else 0
 };
 
@@ -400,7 +402,8 @@ struct ResizeItem {
 // trip each from a far source, while the pull moves the crop window's rows in
 // coalesced 16-byte loads.  `pull` = nullptr: no far sources in this launch.
 __global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_t n,
-                              uint8_t* __restrict__ pull, uint64_t pull_stride) {
+                              uint8_t* __restrict__ pull, uint64_t pull_stride,
+                              uint32_t* __restrict__ far_list, uint32_t* __restrict__ far_count) {
     const uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (k >= n) return;
     uint64_t id;
@@ -412,14 +415,19 @@ __global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_
     it.pitch = a.src.prefix ? var_pitch(W) : 3 * W;
     it.q = aug_params(a.seed, a.epoch, id, H, W, a.out_h, a.out_w, LL_AUG_RESIZE);
     it.from = nullptr;
+    it.to = nullptr;
     it.bytes16 = 0;
     if (far && pull) {
-        // the window's full rows [y0, y0 + ch), widened to 16-byte alignment
+        // the window's full rows [y0, y0 + ch), widened to 16-byte alignment,
+        // into pull slot j (compact: the pull kernel walks far samples only)
         const uint64_t row = it.pitch;
         const uintptr_t start = reinterpret_cast<uintptr_t>(it.src) + it.q.y0 * row;
         const uintptr_t end = start + it.q.ch * row;
         const uintptr_t a16 = start & ~static_cast<uintptr_t>(15);
-        uint8_t* dst = pull + k * pull_stride;
+        const uint32_t j = atomicAdd(far_count, 1u);
+        far_list[j] = static_cast<uint32_t>(k);
+        uint8_t* dst = pull + j * pull_stride;
+        it.to = dst;
         it.from = reinterpret_cast<const uint8_t*>(a16);
         it.bytes16 = static_cast<uint32_t>(((end + 15) & ~static_cast<uintptr_t>(15)) - a16);
         it.src = dst + (start - a16) - it.q.y0 * row;  // same row indexing as the original
@@ -427,20 +435,36 @@ __global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_
     items[k] = it;
 }
 
-constexpr uint32_t kPullCtas = 4;  // CTAs per sample
+// Grid-stride over (far sample, 16 KB unit) pairs: every load of a unit is in
+// flight at once (4 x 16 B per thread), so a step's few far samples cost about
+// one NVLink / PCIe round trip instead of one per 4 KB.
+constexpr uint32_t kPullUnit = 16384;
+constexpr uint32_t kPullCtas = 296;  // 2 per SM
 
 __global__ void __launch_bounds__(256) k_resize_pull(const ResizeItem* __restrict__ items,
-                                                     uint8_t* __restrict__ pull,
-                                                     uint64_t pull_stride) {
-    const uint64_t k = blockIdx.x;
-    const uint8_t* from = items[k].from;
-    if (from == nullptr) return;
-    const uint32_t chunks = items[k].bytes16 / 16;
-    uint4* dst = reinterpret_cast<uint4*>(pull + k * pull_stride);
-    const uint4* src = reinterpret_cast<const uint4*>(from);
-    for (uint32_t c = blockIdx.y * blockDim.x + threadIdx.x; c < chunks;
-         c += kPullCtas * blockDim.x)
-        dst[c] = ld_nc_v4(src + c);
+                                                     const uint32_t* __restrict__ far_list,
+                                                     const uint32_t* __restrict__ far_count,
+                                                     uint32_t units_per_sample) {
+    const uint64_t units = static_cast<uint64_t>(*far_count) * units_per_sample;
+    for (uint64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const uint32_t j = static_cast<uint32_t>(u / units_per_sample);
+        const uint32_t b0 = static_cast<uint32_t>(u - static_cast<uint64_t>(j) * units_per_sample) *
+                            kPullUnit;
+        const ResizeItem& it = items[far_list[j]];
+        if (b0 >= it.bytes16) continue;
+        const uint32_t b1 = b0 + kPullUnit < it.bytes16 ? b0 + kPullUnit : it.bytes16;
+        uint4 v[4];
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+            const uint32_t o = b0 + 16 * (i * blockDim.x + threadIdx.x);
+            if (o < b1) v[i] = ld_nc_v4(it.from + o);
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+            const uint32_t o = b0 + 16 * (i * blockDim.x + threadIdx.x);
+            if (o < b1) *reinterpret_cast<uint4*>(it.to + o) = v[i];
+        }
+    }
 }
 
 // bytes [s, s+4) of the 8-byte pair {hi:lo} (s = sel & 3)
@@ -666,10 +690,9 @@ static void validate_spec(const ll_augment_spec& spec, uint32_t H, uint32_t W) {
     }
 }
 
-void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
-                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out) {
-    validate_spec(spec, height, width);
-    if (n == 0) return;
+static AugArgs make_args(const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
+                         const SrcMap& src, uint64_t n, uint32_t height, uint32_t width,
+                         void* d_out) {
     AugArgs a{};
     a.src = src;
     a.H = height;
@@ -681,6 +704,62 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
     a.n = n;
     a.out_h = spec.out_h;
     a.out_w = spec.out_w;
+    return a;
+}
+
+// The banded resize kernel's limits: 32-bit in-sample offsets, exact 32-bit
+// taps, sources of at least 2 x 2 (a tap pair never leaves the sample).
+// *max_bytes: the largest source sample.
+static bool resize_banded(const ll_augment_spec& spec, const SrcMap& src, uint32_t height,
+                          uint32_t width, uint64_t* max_bytes) {
+    const uint32_t max_side = src.prefix ? kVarMin + kVarSpan - 1 : std::min(height, width);
+    *max_bytes =
+        src.prefix ? 3ull * (kVarMin + kVarSpan) * (kVarMin + kVarSpan) : 3ull * height * width;
+    const uint64_t tap_max = (2ull * std::max(spec.out_h, spec.out_w) + 1) * 64 * max_side;
+    return spec.out_w <= kMaxOutW && tap_max < (1ull << 32) && *max_bytes < (1ull << 31) &&
+           (src.prefix || std::min(height, width) >= 2);
+}
+
+bool resize_prepare(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, int slot) {
+    validate_spec(spec, height, width);
+    uint64_t max_bytes = 0;
+    if (spec.mode != LL_AUG_RESIZE || n == 0 || !resize_banded(spec, src, height, width, &max_bytes))
+        return false;
+    require(n < (1ull << 31), "augment: too many samples in one launch");
+    const std::string tag = std::to_string(slot);
+    const AugArgs a = make_args(spec, seed, epoch, src, n, height, width, nullptr);
+    DevBuf& items = ctx->buf("resize.items" + tag, sizeof(ResizeItem) * n);
+    // far sources possible: peer shards (P2P) or the host storage tier
+    const bool far = src.kind == 1 && (src.peers != nullptr || src.storage != nullptr);
+    const uint64_t pull_stride = (max_bytes + 15) / 16 * 16 + 32;
+    uint8_t* pull = nullptr;
+    uint32_t* fl = nullptr;
+    if (far) {
+        pull = ctx->buf("resize.pull" + tag, n * pull_stride).as<uint8_t>();
+        fl = ctx->buf("resize.far" + tag, sizeof(uint32_t) * (n + 1)).as<uint32_t>();
+        LL_CUDA(cudaMemsetAsync(fl + n, 0, sizeof(uint32_t), ctx->stream));
+    }
+    launch(ctx, "resize_prep", [&] {
+        k_resize_prep<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(
+            a, items.as<ResizeItem>(), n, pull, pull_stride, fl, fl ? fl + n : nullptr);
+    });
+    if (far) {
+        const uint32_t units = static_cast<uint32_t>((max_bytes + 32 + kPullUnit - 1) / kPullUnit);
+        launch(ctx, "resize_pull", [&] {
+            k_resize_pull<<<kPullCtas, 256, 0, ctx->stream>>>(items.as<ResizeItem>(), fl, fl + n,
+                                                              units);
+        });
+    }
+    return true;
+}
+
+void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out,
+                    int prepared_slot) {
+    validate_spec(spec, height, width);
+    if (n == 0) return;
+    const AugArgs a = make_args(spec, seed, epoch, src, n, height, width, d_out);
     const bool bf16 = spec.out_dtype == LL_OUT_BF16;
     if (spec.mode == LL_AUG_CROP) {
         const dim3 grid(static_cast<unsigned>(n * kBands));
@@ -690,61 +769,48 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
             else
                 k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);
         });
-    } else {
-        // banded gather kernel: 32-bit in-sample offsets, exact 32-bit taps,
-        // sources of at least 2 x 2 (a tap pair never leaves the sample)
-        const uint32_t max_side = src.prefix ? kVarMin + kVarSpan - 1 : std::min(height, width);
-        const uint64_t max_bytes =
-            src.prefix ? 3ull * (kVarMin + kVarSpan) * (kVarMin + kVarSpan) : 3ull * height * width;
-        const uint64_t tap_max = (2ull * std::max(spec.out_h, spec.out_w) + 1) * 64 * max_side;
-        if (spec.out_w <= kMaxOutW && tap_max < (1ull << 32) && max_bytes < (1ull << 31) &&
-            (src.prefix || std::min(height, width) >= 2)) {
-            require(n < (1ull << 31), "augment: too many samples in one launch");
-            DevBuf& items = ctx->buf("resize.items", sizeof(ResizeItem) * n);
-            // far sources possible: peer shards (P2P) or the host storage tier
-            const bool far = src.kind == 1 && (src.peers != nullptr || src.storage != nullptr);
-            const uint64_t pull_stride = (max_bytes + 15) / 16 * 16 + 32;
-            uint8_t* pull = far ? ctx->buf("resize.pull", n * pull_stride).as<uint8_t>() : nullptr;
-            launch(ctx, "resize_prep", [&] {
-                k_resize_prep<<<static_cast<unsigned>((n + 127) / 128), 128, 0, ctx->stream>>>(
-                    a, items.as<ResizeItem>(), n, pull, pull_stride);
-            });
-            if (far)
-                launch(ctx, "resize_pull", [&] {
-                    k_resize_pull<<<dim3(static_cast<unsigned>(n), kPullCtas), 256, 0,
-                                    ctx->stream>>>(items.as<ResizeItem>(), pull, pull_stride);
-                });
-            const dim3 grid(static_cast<unsigned>(n), (spec.out_h + kRB - 1) / kRB);
-            const unsigned threads = 32 * ((spec.out_w + 31) / 32);
-            // word-aligned rows: the variable-geometry shard layout (geometry.cuh)
-            const bool aligned = src.prefix != nullptr;
-            launch(ctx, "augment_resize", [&] {
-                const ResizeItem* it = items.as<ResizeItem>();
-                const bool out224 = spec.out_h == 224 && spec.out_w == 224;
-                if (bf16 && aligned && out224)
-                    k_augment_resize_rows<true, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
-                else if (!bf16 && aligned && out224)
-                    k_augment_resize_rows<false, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
-                else if (bf16 && aligned)
-                    k_augment_resize_rows<true, true><<<grid, threads, 0, ctx->stream>>>(a, it);
-                else if (bf16)
-                    k_augment_resize_rows<true, false><<<grid, threads, 0, ctx->stream>>>(a, it);
-                else if (aligned)
-                    k_augment_resize_rows<false, true><<<grid, threads, 0, ctx->stream>>>(a, it);
-                else
-                    k_augment_resize_rows<false, false><<<grid, threads, 0, ctx->stream>>>(a, it);
-            });
-            return;
-        }
-        require(src.prefix == nullptr, "augment: variable geometry needs the banded resize kernel");
-        const dim3 grid(static_cast<unsigned>(n * spec.out_h));
-        launch(ctx, "augment_resize", [&] {
-            if (bf16)
-                k_augment_resize<true><<<grid, 256, 0, ctx->stream>>>(a);
-            else
-                k_augment_resize<false><<<grid, 256, 0, ctx->stream>>>(a);
-        });
+        return;
     }
+    uint64_t max_bytes = 0;
+    if (resize_banded(spec, src, height, width, &max_bytes)) {
+        // the prologue (K7 prep + far pull) ran already (the loader prefetches
+        // it on its side stream into sets 0/1) or runs now into set 2
+        int slot = prepared_slot;
+        if (slot < 0) {
+            resize_prepare(ctx, spec, seed, epoch, src, n, height, width, 2);
+            slot = 2;
+        }
+        const ResizeItem* it = ctx->buf("resize.items" + std::to_string(slot),
+                                        sizeof(ResizeItem) * n).as<ResizeItem>();
+        const dim3 grid(static_cast<unsigned>(n), (spec.out_h + kRB - 1) / kRB);
+        const unsigned threads = 32 * ((spec.out_w + 31) / 32);
+        // word-aligned rows: the variable-geometry shard layout (geometry.cuh)
+        const bool aligned = src.prefix != nullptr;
+        const bool out224 = spec.out_h == 224 && spec.out_w == 224;
+        launch(ctx, "augment_resize", [&] {
+            if (bf16 && aligned && out224)
+                k_augment_resize_rows<true, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
+            else if (!bf16 && aligned && out224)
+                k_augment_resize_rows<false, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
+            else if (bf16 && aligned)
+                k_augment_resize_rows<true, true><<<grid, threads, 0, ctx->stream>>>(a, it);
+            else if (bf16)
+                k_augment_resize_rows<true, false><<<grid, threads, 0, ctx->stream>>>(a, it);
+            else if (aligned)
+                k_augment_resize_rows<false, true><<<grid, threads, 0, ctx->stream>>>(a, it);
+            else
+                k_augment_resize_rows<false, false><<<grid, threads, 0, ctx->stream>>>(a, it);
+        });
+        return;
+    }
+    require(src.prefix == nullptr, "augment: variable geometry needs the banded resize kernel");
+    const dim3 grid(static_cast<unsigned>(n * spec.out_h));
+    launch(ctx, "augment_resize", [&] {
+        if (bf16)
+            k_augment_resize<true><<<grid, 256, 0, ctx->stream>>>(a);
+        else
+            k_augment_resize<false><<<grid, 256, 0, ctx->stream>>>(a);
+    });
 }
 
 void augment_params_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed,

@@ -209,8 +209,14 @@ struct SrcMap {
     // a mapped pinned host buffer read over PCIe / C2C by the kernel itself
     const uint8_t* storage = nullptr;
 };
+// prepared_slot >= 0: the resize prologue already ran into that buffer set
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
-                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out);
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out,
+                    int prepared_slot = -1);
+// Resize prologue (per-sample geometry, far-sample pull) into buffer set
+// `slot` on ctx->stream; false when the step has no banded-resize prologue.
+bool resize_prepare(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, int slot);
 void augment_params_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed,
                            uint64_t epoch, const uint64_t* d_ids, uint64_t n, uint32_t height,
                            uint32_t width, uint32_t* d_params5);

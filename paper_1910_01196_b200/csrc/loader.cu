@@ -84,6 +84,10 @@ struct ll_loader {
         bool valid = false;
         uint64_t epoch = 0, step = 0;
     } xpending[2];
+    // resize prologue (K7 prep + far pull) of step t+1 issued on the side
+    // stream while step t's augment runs (buffer sets 0/1 by step parity)
+    cudaEvent_t rready[2] = {nullptr, nullptr}, rdone[2] = {nullptr, nullptr};
+    Pending rpending[2];
     std::vector<void*> peer_open;  // opened IPC mappings (excluding self)
     ll::DevBuf d_peers;
     bool peers_ready = false;
@@ -231,26 +235,30 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
     LL_NCCL(ncclGroupEnd());
 }
 
-void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
-              const ll_move* h_moves, const uint32_t* h_off, const uint32_t* h_kept,
-              uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info,
-              const uint8_t* prefetched_recv = nullptr) {
-    ll_ctx* ctx = ld->ctx;
+// Where this learner's samples of `step` come from (own shard, storage tier,
+// peer shards), for every exchange but NCCL (run_step adds the receive buffer).
+struct StepSrc {
+    SrcMap src;
+    uint64_t n_local = 0, n_send = 0, n_recv = 0, nvl_recv = 0;
+};
+
+StepSrc step_src(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_move* h_moves,
+                 const uint32_t* h_off, const uint32_t* h_kept, uint32_t h_nmoves) {
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
     const uint64_t B = c.batch_size;
     const uint32_t* d_final_step = pd.final_ids + step * B;
-    const uint64_t n_local = h_off[me + 1] - h_off[me];
+    StepSrc r;
+    r.n_local = h_off[me + 1] - h_off[me];
     const uint64_t kept = h_kept[me];
-    uint64_t n_send = 0, n_recv = 0, nvl_recv = 0;
     for (uint32_t m = 0; m < h_nmoves; ++m) {
-        if (h_moves[m].sender == me) n_send += h_moves[m].count;
+        if (h_moves[m].sender == me) r.n_send += h_moves[m].count;
         if (h_moves[m].receiver == me) {
-            n_recv += h_moves[m].count;
-            nvl_recv += h_moves[m].nvlink;
+            r.n_recv += h_moves[m].count;
+            r.nvl_recv += h_moves[m].nvlink;
         }
     }
-    SrcMap src;
+    SrcMap& src = r.src;
     src.kind = 1;
     src.list = d_final_step + h_off[me];
     src.kept = static_cast<uint32_t>(kept);
@@ -272,29 +280,53 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
                 "loader: the regular scheme needs the P2P exchange (peer shards)");
         src.kept = 0;
         src.peers = ld->d_peers.as<const uint8_t*>();
-        n_recv = n_local;
-    } else if (p > 1 && (n_send || n_recv)) {
-        if (c.exchange == LL_EXCHANGE_NCCL) {
-            if (prefetched_recv) {
-                src.recv = prefetched_recv;
-            } else {
-                issue_exchange(ld, pd, step, h_moves, h_nmoves, h_off, ld->packbuf, ld->recvbuf,
-                               ctx->stream);
-                src.recv = ld->recvbuf.as<uint8_t>();
-            }
-        } else if (c.exchange == LL_EXCHANGE_P2P) {
+        r.n_recv = r.n_local;
+    } else if (p > 1 && (r.n_send || r.n_recv)) {
+        if (c.exchange == LL_EXCHANGE_P2P) {
             require(ld->peers_ready, "loader: P2P exchange needs peer shards (open/link)");
             src.peers = ld->d_peers.as<const uint8_t*>();
-        } else {
+        } else if (c.exchange != LL_EXCHANGE_NCCL) {
             fail(LL_ERR_INVALID, "loader: remote samples need an exchange (NCCL or P2P)");
+        }
+    }
+    return r;
+}
+
+uint32_t geom_h(const ll_loader_config& c) {
+    return c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.height;
+}
+uint32_t geom_w(const ll_loader_config& c) {
+    return c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.width;
+}
+
+// prepared_slot >= 0: the resize prologue of this step is in that buffer set
+void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
+              const ll_move* h_moves, const uint32_t* h_off, const uint32_t* h_kept,
+              uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info,
+              const uint8_t* prefetched_recv = nullptr, int prepared_slot = -1) {
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const uint32_t me = c.rank, p = c.learners;
+    const uint64_t B = c.batch_size;
+    const uint32_t* d_final_step = pd.final_ids + step * B;
+    StepSrc ss = step_src(ld, pd, step, h_moves, h_off, h_kept, h_nmoves);
+    SrcMap& src = ss.src;
+    const uint64_t n_local = ss.n_local, n_recv = ss.n_recv, nvl_recv = ss.nvl_recv;
+    if (p > 1 && c.scheme != LL_SCHEME_REGULAR && (ss.n_send || ss.n_recv) &&
+        c.exchange == LL_EXCHANGE_NCCL) {
+        if (prefetched_recv) {
+            src.recv = prefetched_recv;
+        } else {
+            issue_exchange(ld, pd, step, h_moves, h_nmoves, h_off, ld->packbuf, ld->recvbuf,
+                           ctx->stream);
+            src.recv = ld->recvbuf.as<uint8_t>();
         }
     }
     ensure_out(ld);
     void* out = ld->out[ld->out_slot]->ptr;
     ld->out_slot = (ld->out_slot + 1) % ld->out.size();
-    const uint32_t gh = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.height;
-    const uint32_t gw = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.width;
-    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, gh, gw, out);
+    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, geom_h(c), geom_w(c), out,
+                   prepared_slot);
     if (info) {
         info->epoch = epoch;
         info->step = step;
@@ -466,6 +498,8 @@ void loader_destroy(ll_loader* ld) {
     if (ld->side) cudaStreamDestroy(ld->side);
     for (int i = 0; i < 2; ++i) {
         if (ld->xdone[i]) cudaEventDestroy(ld->xdone[i]);
+        if (ld->rready[i]) cudaEventDestroy(ld->rready[i]);
+        if (ld->rdone[i]) cudaEventDestroy(ld->rdone[i]);
         if (ld->augdone[i]) cudaEventDestroy(ld->augdone[i]);
     }
     if (ld->storage) cudaFreeHost(ld->storage);
@@ -561,6 +595,7 @@ void populate_storage(ll_loader* ld) {
 }
 
 void ensure_plan_stream(ll_loader* ld);
+void ensure_side_stream(ll_loader* ld);
 
 // Steady state from the first step on: the output ring, the plan stream and
 // the second plan slot (device scratch, pinned host tables) are created here,
@@ -569,6 +604,7 @@ void ensure_plan_stream(ll_loader* ld);
 void prime(ll_loader* ld) {
     ensure_out(ld);
     ensure_plan_stream(ld);
+    ensure_side_stream(ld);
     if (ld->slot[1].epoch < 0) {
         plan_into(ld, 1, 1, ld->plan_stream);
         LL_CUDA(cudaStreamSynchronize(ld->plan_stream));
@@ -768,6 +804,8 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     for (int i = 0; i < 2; ++i) {
         if (ld->xdone[i]) LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[i], 0));
         ld->xpending[i].valid = false;
+        if (ld->rready[i]) LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->rready[i], 0));
+        ld->rpending[i].valid = false;
     }
     const int k = ld->plan_epoch >= 0 ? ld->cur ^ 1 : ld->cur;
     auto& sl = ld->slot[k];
@@ -874,9 +912,61 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
         pend.valid = false;
         pre = ld->xrecv[slot].as<uint8_t>();
     }
+    // resize (K7): the prologue of this step was prefetched under the previous
+    // step's augment, or runs now; that of the next step is issued after it
+    const bool rpre = c.augment.mode == LL_AUG_RESIZE && !nccl;
+    int pslot = -1;
+    if (rpre) {
+        if (!ld->rready[0]) {
+            for (int i = 0; i < 2; ++i) {
+                LL_CUDA(cudaEventCreateWithFlags(&ld->rready[i], cudaEventDisableTiming));
+                LL_CUDA(cudaEventCreateWithFlags(&ld->rdone[i], cudaEventDisableTiming));
+            }
+            ensure_side_stream(ld);
+        }
+        const int rs = static_cast<int>(step & 1);
+        auto& rp = ld->rpending[rs];
+        // any side-stream write into this set has landed before it is read or rewritten
+        LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->rready[rs], 0));
+        if (rp.valid && rp.epoch == epoch && rp.step == step) {
+            pslot = rs;
+        } else {
+            auto [mv, off, kept, nm, st] = tables(step);
+            (void)st;
+            const StepSrc ss = step_src(ld, ld->plan().view(), step, mv, off, kept, nm);
+            if (resize_prepare(ctx, c.augment, c.seed, epoch, ss.src, ss.n_local, geom_h(c),
+                               geom_w(c), rs))
+                pslot = rs;
+        }
+        rp.valid = false;
+    }
     {
         auto [mv, off, kept, nm, st] = tables(step);
-        run_step(ld, epoch, ld->plan().view(), step, mv, off, kept, nm, st, info, pre);
+        run_step(ld, epoch, ld->plan().view(), step, mv, off, kept, nm, st, info, pre, pslot);
+    }
+    if (rpre) {
+        LL_CUDA(cudaEventRecord(ld->rdone[step & 1], ctx->stream));
+        if (step + 1 < ld->steps) {
+            const int ns = static_cast<int>((step + 1) & 1);
+            auto [mv, off, kept, nm, st] = tables(step + 1);
+            (void)st;
+            const StepSrc ss = step_src(ld, ld->plan().view(), step + 1, mv, off, kept, nm);
+            // set ns was last read by step - 1's augment
+            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->rdone[ns], 0));
+            cudaStream_t main = ctx->stream;
+            ctx->stream = ld->side;
+            bool ok = false;
+            try {
+                ok = resize_prepare(ctx, c.augment, c.seed, epoch, ss.src, ss.n_local, geom_h(c),
+                                    geom_w(c), ns);
+            } catch (...) {
+                ctx->stream = main;
+                throw;
+            }
+            ctx->stream = main;
+            LL_CUDA(cudaEventRecord(ld->rready[ns], ld->side));
+            ld->rpending[ns] = {ok, epoch, step + 1};
+        }
     }
     // halfway through the epoch, start the next epoch's plan on its own stream
     if (step == ld->steps / 2) prefetch_plan(ld, epoch + 1);
