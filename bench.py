@@ -64,7 +64,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
-    ap.add_argument("--prefetch-depth", type=int, default=2,
+    ap.add_argument("--prefetch-depth", type=int, default=4,
                     help="LoaderConfig::prefetch_depth (output ring / host steps in flight)")
     args = ap.parse_args()
     if args.dtype is None:

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
     __shared__ uint32_t mv_nvl[kMaxP];
     __shared__ uint32_t reg_remote;
     __shared__ long long imb[kMaxP];
+    __shared__ uint32_t rc[kMaxP * kMaxP];  // regular + NCCL: [slice][owner] counts
 
     uint32_t* scratch = P.scratch + st * B;
     uint32_t* final_ids = P.final_ids + st * B;
@@ -96,6 +97,9 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
     if (tid <= p) total[tid] = 0;
     if (tid < kMaxP) mv_nvl[tid] = 0;
     if (tid == 0) reg_remote = 0;
+    const bool want_rc = slice && P.regcnt != nullptr;
+    if (want_rc)
+        for (uint32_t i = tid; i < p * p; i += kThreads) rc[i] = 0;
     __syncthreads();
 
     // ---- pass 1: stable rank of every sample inside its owner group -------
@@ -108,6 +112,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
             const uint64_t s = batch[e];
             g = s < a.cached ? static_cast<uint32_t>(s * p / a.cached) : p;
             if (slice && g != static_cast<uint32_t>(e / slice) && g < p) ++my_reg_remote;
+            if (want_rc && g < p) atomicAdd(&rc[static_cast<uint32_t>(e / slice) * p + g], 1u);
         }
         const unsigned peers = __match_any_sync(0xffffffffu, g);
         const uint32_t lrank = __popc(peers & ((1u << lane) - 1u));
@@ -206,6 +211,8 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
     __syncthreads();
 
     // ---- plan records -------------------------------------------------------
+    if (want_rc)
+        for (uint32_t i = tid; i < p * p; i += kThreads) P.regcnt[st * p * p + i] = rc[i];
     if (tid <= p) P.off[st * (kMaxP + 1) + tid] = off[tid];
     if (tid < p) {
         P.kept[st * kMaxP + tid] = kept[tid];
@@ -256,7 +263,12 @@ PlanDev PlanBufs::view() const {
     v.stats = stats.as<uint32_t>();
     v.scratch = scratch.as<uint32_t>();
     v.aug = aug.as<uint32_t>();
+    v.regcnt = regcnt.as<uint32_t>();
     return v;
+}
+
+void PlanBufs::reserve_regcnt(uint64_t steps, uint32_t p) {
+    regcnt.reserve(sizeof(uint32_t) * steps * p * p);
 }
 
 void PlanBufs::reserve(uint64_t steps, uint64_t B) {

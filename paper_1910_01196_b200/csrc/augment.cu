@@ -76,6 +76,15 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
     const uint32_t kept = m.kept_dev ? *m.kept_dev : m.kept;
     const uint64_t s = list[k];
     *id = s;
+    if (m.recv_idx) {  // regular scheme over NCCL
+        const uint32_t ri = m.recv_idx[k];
+        if (ri == 0xFFFFFFFFu) {
+            *src = m.shard + (s - m.shard_first) * m.sample_bytes;
+        } else {
+            *src = m.recv + static_cast<uint64_t>(ri) * m.sample_bytes;
+        }
+        return;
+    }
     if (s >= m.cached && m.storage) {
         // storage tier (alpha < 1): uncached samples from mapped pinned host memory
         *src = m.storage + (s - m.cached) * m.sample_bytes;

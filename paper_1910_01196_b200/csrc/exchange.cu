@@ -45,7 +45,69 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
     }
 }
 
+// Regular scheme (reg_slice, sampling.cpp:27-42) over NCCL: learner j's slice
+// is batch positions [j*L, (j+1)*L) in batch order, and every sample is read
+// from its owner.  The pair (slice j, owner o) exchanges regcnt[j][o] samples;
+// a sample's index inside that message is its rank among the owner-o samples
+// of slice j (its rank in the owner's whole-batch group, scratch[e] from K4
+// pass 1, minus the owner-o samples of earlier slices).  One CTA per batch
+// position: the sender copies its own samples of other slices into their
+// message (pack segment j of L samples), the receiver records for each slice
+// position the receive-segment index, or kLocal for its own samples.
+constexpr uint32_t kLocal = 0xFFFFFFFFu;
+
+struct RegPrepArgs {
+    const uint32_t* batch;    // final ids of the step (regular: the batch itself)
+    const uint32_t* scratch;  // K4 pass 1: owner << 24 | rank in the owner's batch group
+    const uint32_t* regcnt;   // [p][p] of the step
+    uint32_t p, me, L;
+    const uint8_t* shard;
+    uint64_t shard_first, sample_bytes;
+    uint8_t* pack;            // [p][L] samples
+    uint32_t* ridx;           // [L]: my slice position -> receive index or kLocal
+};
+
+__global__ void __launch_bounds__(256) k_reg_prep(RegPrepArgs a) {
+    const uint32_t e = blockIdx.x;
+    const uint32_t j = e / a.L;
+    const uint32_t v = a.scratch[e];
+    const uint32_t o = v >> 24;
+    if (j != a.me && o != a.me) return;  // neither mine to send nor in my slice
+    __shared__ uint32_t s_rank;
+    if (threadIdx.x == 0) {
+        uint32_t before = 0;
+        for (uint32_t jj = 0; jj < j; ++jj) before += a.regcnt[jj * a.p + o];
+        s_rank = (v & 0xFFFFFFu) - before;
+    }
+    __syncthreads();
+    const uint32_t rank = s_rank;
+    if (j == a.me) {
+        if (threadIdx.x == 0) a.ridx[e - j * a.L] = o == a.me ? kLocal : o * a.L + rank;
+        return;
+    }
+    // o == me, j != me: copy the sample into message (j), slot rank
+    const uint32_t id = a.batch[e];
+    const uint4* src = reinterpret_cast<const uint4*>(a.shard + (id - a.shard_first) * a.sample_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(a.pack + (static_cast<uint64_t>(j) * a.L + rank) *
+                                                       a.sample_bytes);
+    const uint64_t n16 = a.sample_bytes / 16;
+    for (uint64_t c = threadIdx.x; c < n16; c += blockDim.x) __stcs(dst + c, __ldg(src + c));
+}
+
 } // namespace
+
+void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scratch,
+                     const uint32_t* d_regcnt, uint32_t p, uint32_t me, uint64_t B,
+                     const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
+                     uint8_t* pack, uint32_t* ridx) {
+    require(sample_bytes % 16 == 0, "exchange: sample bytes must be a multiple of 16");
+    require(B % p == 0, "reg_slice: learner count must divide the batch size");
+    RegPrepArgs a{d_batch, d_scratch, d_regcnt, p, me, static_cast<uint32_t>(B / p), shard,
+                  shard_first, sample_bytes, pack, ridx};
+    launch(ctx, "reg_prep", [&] {
+        k_reg_prep<<<static_cast<unsigned>(B), 256, 0, ctx->stream>>>(a);
+    });
+}
 
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,

@@ -146,6 +146,9 @@ struct PlanDev {
     uint32_t* stats = nullptr;      // [steps][4]: moved, nvlink, uncached, reg_remote
     uint32_t* scratch = nullptr;    // [steps][B]
     uint32_t* aug = nullptr;        // [steps][B] packed crop params per final slot (or null)
+    // regular scheme with the NCCL exchange (or null): [steps][p][p] samples
+    // of slice j owned by learner o at [j * p + o]
+    uint32_t* regcnt = nullptr;
 };
 // Crop parameters the plan precomputes for every final slot (crop mode):
 // packed y0 | x0 << 15 | flip << 31 (lo_aug_params_for).
@@ -155,9 +158,10 @@ struct AugPlan {
     uint32_t H = 0, W = 0, ch = 0, cw = 0;
 };
 struct PlanBufs {
-    DevBuf final_ids, off, kept, counts, moves, n_moves, stats, scratch, aug;
+    DevBuf final_ids, off, kept, counts, moves, n_moves, stats, scratch, aug, regcnt;
     PlanDev view() const;
     void reserve(uint64_t steps, uint64_t B);
+    void reserve_regcnt(uint64_t steps, uint32_t p);
 };
 void assign_device(ll_ctx* ctx, const uint32_t* d_order, uint64_t steps, uint64_t B, uint32_t p,
                    uint64_t cached, int scheme, const PlanDev& plan,
@@ -208,6 +212,8 @@ struct SrcMap {
     // storage tier (alpha < 1): sample s >= cached at storage + (s - cached) * bytes,
     // a mapped pinned host buffer read over PCIe / C2C by the kernel itself
     const uint8_t* storage = nullptr;
+    // regular scheme over NCCL: list position -> recv index (0xFFFFFFFF: own shard)
+    const uint32_t* recv_idx = nullptr;
 };
 // prepared_slot >= 0: the resize prologue already ran into that buffer set
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
@@ -226,6 +232,13 @@ std::vector<ll_xfer> exchange_plan(const ll_move* moves, uint32_t n, const uint3
                                    uint32_t me);
 std::vector<ll_xfer> exchange_plan(const ll_move* moves, uint32_t n, const uint64_t* off,
                                    uint32_t me);
+// regular scheme over NCCL: pack this learner's samples of other slices into
+// [p][B/p] messages, and map its own slice positions to receive indices
+// (0xFFFFFFFF = own shard)
+void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scratch,
+                     const uint32_t* d_regcnt, uint32_t p, uint32_t me, uint64_t B,
+                     const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
+                     uint8_t* pack, uint32_t* ridx);
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
                  uint8_t* packbuf);

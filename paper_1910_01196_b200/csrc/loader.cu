@@ -64,6 +64,7 @@ struct ll_loader {
         ll_move* moves = nullptr;    // pinned host tables
         uint32_t *off = nullptr, *kept = nullptr, *counts = nullptr, *nmoves = nullptr,
                  *stats = nullptr;
+        uint32_t* regcnt = nullptr;  // regular + NCCL: [steps][p][p]
     } slot[2];
     int cur = 0;
     cudaStream_t plan_stream = nullptr;
@@ -71,14 +72,19 @@ struct ll_loader {
     ll::PlanBufs& plan() { return slot[cur].plan; }
     // current epoch's host tables
     ll_move* h_moves = nullptr;
+    uint32_t* h_regcnt = nullptr;  // regular + NCCL: [steps][p][p]
     uint32_t *h_off = nullptr, *h_kept = nullptr, *h_counts = nullptr, *h_nmoves = nullptr,
              *h_stats = nullptr;
     // exchange
     ncclComm_t comm = nullptr;
-    ll::DevBuf packbuf, recvbuf;
+    // one step's exchange buffers: send messages, receive buffer and, for the
+    // regular scheme, the slice-position -> receive-index map
+    struct ExSet {
+        ll::DevBuf pack, recv, ridx;
+    } xcur;
     // NCCL exchange of step t+1 issued on the side stream while step t's
     // augment runs (two buffer sets, alternating by step parity)
-    ll::DevBuf xpack[2], xrecv[2];
+    ExSet xset[2];
     cudaEvent_t xdone[2] = {nullptr, nullptr}, augdone[2] = {nullptr, nullptr};
     struct Pending {
         bool valid = false;
@@ -128,6 +134,11 @@ uint64_t out_elem_bytes(const ll_loader_config& c) {
 
 // Queue the D2H of slot `k`'s step tables on `stream` (pinned destination) and
 // mark the slot's ready event.
+// the regular scheme's full-volume exchange over NCCL
+bool reg_nccl(const ll_loader_config& c) {
+    return c.learners > 1 && c.scheme == LL_SCHEME_REGULAR && c.exchange == LL_EXCHANGE_NCCL;
+}
+
 void copy_tables(ll_loader* ld, int k, cudaStream_t stream) {
     auto& sl = ld->slot[k];
     const uint64_t steps = ld->steps;
@@ -141,6 +152,10 @@ void copy_tables(ll_loader* ld, int k, cudaStream_t stream) {
     d2h(sl.counts, plan.counts, sizeof(uint32_t) * steps * kMaxP);
     d2h(sl.nmoves, plan.n_moves, sizeof(uint32_t) * steps);
     d2h(sl.stats, plan.stats, sizeof(uint32_t) * steps * 4);
+    if (sl.regcnt) {
+        const uint64_t p = ld->cfg.learners;
+        d2h(sl.regcnt, plan.regcnt, sizeof(uint32_t) * steps * p * p);
+    }
     LL_CUDA(cudaEventRecord(sl.ready, stream));
 }
 
@@ -195,42 +210,76 @@ void ensure_out(ll_loader* ld) {
     }
 }
 
-// Issue exchange + augment of one step whose plan tables are at (plan, step)
-// with host mirrors (h_*, index hs).
-// K5 pack + one grouped NCCL send/recv of step `step` on `stream`; received
-// samples land in `recv` in the learner's final-list order.
+// One step's exchange on `stream`, NCCL grouped send/recv.
+//  * balanced / locality schemes: K5 packs the tail moves this learner sends
+//    (Algorithm 1 + equivalence.cpp:77-88); received samples land in x.recv
+//    in the learner's final-list order;
+//  * regular scheme (reg_slice, sampling.cpp:27-42): every learner exchanges
+//    with every other its owned samples of their slices (h_regcnt: this
+//    step's [slice][owner] counts); x.ridx maps slice positions to x.recv.
 void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_move* h_moves,
-                    uint32_t h_nmoves, const uint32_t* h_off, DevBuf& pack, DevBuf& recv,
-                    cudaStream_t stream) {
+                    uint32_t h_nmoves, const uint32_t* h_off, const uint32_t* h_regcnt,
+                    ll_loader::ExSet& x, cudaStream_t stream) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
-    const uint32_t me = c.rank;
+    const uint32_t me = c.rank, p = c.learners;
+    const uint64_t B = c.batch_size;
     require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
     require(c.geometry == LL_GEOM_FIXED, "loader: variable-size samples need the P2P exchange");
-    const uint32_t* d_final_step = pd.final_ids + step * c.batch_size;
+    const uint32_t* d_final_step = pd.final_ids + step * B;
+    cudaStream_t main = ctx->stream;
+    if (c.scheme == LL_SCHEME_REGULAR) {
+        require(h_regcnt != nullptr && pd.regcnt != nullptr, "loader: regular plan lacks counts");
+        const uint64_t L = B / p;
+        x.pack.reserve(B * ld->S);
+        x.recv.reserve(B * ld->S);
+        x.ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(L, 1));
+        ctx->stream = stream;
+        try {
+            reg_prep_device(ctx, d_final_step, pd.scratch + step * B, pd.regcnt + step * p * p, p,
+                            me, B, ld->shard.as<uint8_t>(), ld->first, ld->S,
+                            x.pack.as<uint8_t>(), x.ridx.as<uint32_t>());
+        } catch (...) {
+            ctx->stream = main;
+            throw;
+        }
+        ctx->stream = main;
+        LL_NCCL(ncclGroupStart());
+        for (uint32_t r = 0; r < p; ++r) {
+            if (r == me) continue;
+            const uint64_t ns = h_regcnt[r * p + me], nr = h_regcnt[me * p + r];
+            if (ns)
+                LL_NCCL(ncclSend(x.pack.as<uint8_t>() + r * L * ld->S, ns * ld->S, ncclUint8,
+                                 static_cast<int>(r), ld->comm, stream));
+            if (nr)
+                LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + r * L * ld->S, nr * ld->S, ncclUint8,
+                                 static_cast<int>(r), ld->comm, stream));
+        }
+        LL_NCCL(ncclGroupEnd());
+        return;
+    }
     const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
     uint64_t n_send = 0, n_recv = 0;
-    for (const ll_xfer& x : xs) (x.is_send ? n_send : n_recv) += x.count;
-    pack.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
-    recv.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
-    cudaStream_t main = ctx->stream;
+    for (const ll_xfer& xf : xs) (xf.is_send ? n_send : n_recv) += xf.count;
+    x.pack.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
+    x.recv.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
     ctx->stream = stream;  // pack_device launches on the context stream
     try {
         pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
-                    pack.as<uint8_t>());
+                    x.pack.as<uint8_t>());
     } catch (...) {
         ctx->stream = main;
         throw;
     }
     ctx->stream = main;
     LL_NCCL(ncclGroupStart());
-    for (const ll_xfer& x : xs) {
-        if (x.is_send)
-            LL_NCCL(ncclSend(pack.as<uint8_t>() + x.buf_first * ld->S, x.count * ld->S, ncclUint8,
-                             static_cast<int>(x.peer), ld->comm, stream));
+    for (const ll_xfer& xf : xs) {
+        if (xf.is_send)
+            LL_NCCL(ncclSend(x.pack.as<uint8_t>() + xf.buf_first * ld->S, xf.count * ld->S,
+                             ncclUint8, static_cast<int>(xf.peer), ld->comm, stream));
         else
-            LL_NCCL(ncclRecv(recv.as<uint8_t>() + x.buf_first * ld->S, x.count * ld->S, ncclUint8,
-                             static_cast<int>(x.peer), ld->comm, stream));
+            LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + xf.buf_first * ld->S, xf.count * ld->S,
+                             ncclUint8, static_cast<int>(xf.peer), ld->comm, stream));
     }
     LL_NCCL(ncclGroupEnd());
 }
@@ -275,11 +324,13 @@ StepSrc step_src(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_move*
     if (c.augment.mode == LL_AUG_CROP) src.aug = pd.aug + step * B + h_off[me];
     if (p > 1 && c.scheme == LL_SCHEME_REGULAR) {
         // reg_slice (sampling.cpp:27-42) ignores ownership: every sample of the
-        // slice is read from its owner's shard (the owner may be this learner).
-        require(c.exchange == LL_EXCHANGE_P2P && ld->peers_ready,
-                "loader: the regular scheme needs the P2P exchange (peer shards)");
+        // slice is read from its owner's shard (the owner may be this learner),
+        // over P2P, or received over NCCL (run_step adds the receive buffer)
+        require((c.exchange == LL_EXCHANGE_P2P && ld->peers_ready) ||
+                    c.exchange == LL_EXCHANGE_NCCL,
+                "loader: the regular scheme needs an exchange (P2P peer shards or NCCL)");
         src.kept = 0;
-        src.peers = ld->d_peers.as<const uint8_t*>();
+        if (c.exchange == LL_EXCHANGE_P2P) src.peers = ld->d_peers.as<const uint8_t*>();
         r.n_recv = r.n_local;
     } else if (p > 1 && (r.n_send || r.n_recv)) {
         if (c.exchange == LL_EXCHANGE_P2P) {
@@ -303,7 +354,8 @@ uint32_t geom_w(const ll_loader_config& c) {
 void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
               const ll_move* h_moves, const uint32_t* h_off, const uint32_t* h_kept,
               uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info,
-              const uint8_t* prefetched_recv = nullptr, int prepared_slot = -1) {
+              const ll_loader::ExSet* prefetched = nullptr, int prepared_slot = -1,
+              const uint32_t* h_regcnt = nullptr) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
@@ -311,15 +363,20 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     const uint32_t* d_final_step = pd.final_ids + step * B;
     StepSrc ss = step_src(ld, pd, step, h_moves, h_off, h_kept, h_nmoves);
     SrcMap& src = ss.src;
-    const uint64_t n_local = ss.n_local, n_recv = ss.n_recv, nvl_recv = ss.nvl_recv;
-    if (p > 1 && c.scheme != LL_SCHEME_REGULAR && (ss.n_send || ss.n_recv) &&
-        c.exchange == LL_EXCHANGE_NCCL) {
-        if (prefetched_recv) {
-            src.recv = prefetched_recv;
-        } else {
-            issue_exchange(ld, pd, step, h_moves, h_nmoves, h_off, ld->packbuf, ld->recvbuf,
+    const uint64_t n_local = ss.n_local;
+    uint64_t n_recv = ss.n_recv, nvl_recv = ss.nvl_recv;
+    const bool reg = p > 1 && c.scheme == LL_SCHEME_REGULAR;
+    if (p > 1 && c.exchange == LL_EXCHANGE_NCCL && (reg || ss.n_send || ss.n_recv)) {
+        const ll_loader::ExSet* x = prefetched;
+        if (!x) {
+            issue_exchange(ld, pd, step, h_moves, h_nmoves, h_off, h_regcnt, ld->xcur,
                            ctx->stream);
-            src.recv = ld->recvbuf.as<uint8_t>();
+            x = &ld->xcur;
+        }
+        src.recv = x->recv.as<uint8_t>();
+        if (reg) {
+            src.recv_idx = x->ridx.as<uint32_t>();
+            n_recv = nvl_recv = n_local - h_regcnt[me * p + me];
         }
     }
     ensure_out(ld);
@@ -479,6 +536,11 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
         LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.counts), sizeof(uint32_t) * st * kMaxP, 0));
         LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.nmoves), sizeof(uint32_t) * st, 0));
         LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.stats), sizeof(uint32_t) * st * 4, 0));
+        if (reg_nccl(c)) {
+            sl.plan.reserve_regcnt(st, c.learners);
+            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&sl.regcnt),
+                                  sizeof(uint32_t) * st * c.learners * c.learners, 0));
+        }
         LL_CUDA(cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
     }
     *out = ld.release();
@@ -506,7 +568,8 @@ void loader_destroy(ll_loader* ld) {
     for (auto& sl : ld->slot) {
         for (void* q : {static_cast<void*>(sl.moves), static_cast<void*>(sl.off),
                         static_cast<void*>(sl.kept), static_cast<void*>(sl.counts),
-                        static_cast<void*>(sl.nmoves), static_cast<void*>(sl.stats)})
+                        static_cast<void*>(sl.nmoves), static_cast<void*>(sl.stats),
+                        static_cast<void*>(sl.regcnt)})
             if (q) cudaFreeHost(q);
         if (sl.ready) cudaEventDestroy(sl.ready);
     }
@@ -824,6 +887,7 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
     ld->h_counts = sl.counts;
     ld->h_nmoves = sl.nmoves;
     ld->h_stats = sl.stats;
+    ld->h_regcnt = sl.regcnt;
     ld->plan_epoch = static_cast<int64_t>(epoch);
 }
 
@@ -878,13 +942,16 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
     set_device(ld->ctx);
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
-    const bool nccl = c.learners > 1 && c.exchange == LL_EXCHANGE_NCCL &&
-                      c.scheme != LL_SCHEME_REGULAR;
+    const bool nccl = c.learners > 1 && c.exchange == LL_EXCHANGE_NCCL;
     auto tables = [&](uint64_t st) {
         return std::make_tuple(&ld->h_moves[st * kMaxP], &ld->h_off[st * (kMaxP + 1)],
                                &ld->h_kept[st * kMaxP], ld->h_nmoves[st], &ld->h_stats[st * 4]);
     };
-    const uint8_t* pre = nullptr;
+    const uint64_t pp = static_cast<uint64_t>(c.learners) * c.learners;
+    auto regcnt = [&](uint64_t st) -> const uint32_t* {
+        return ld->h_regcnt ? ld->h_regcnt + st * pp : nullptr;
+    };
+    const ll_loader::ExSet* pre = nullptr;
     const uint32_t slot = step & 1;
     if (nccl) {
         if (!ld->xdone[0]) {
@@ -904,13 +971,13 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             auto [mv, off, kept, nm, st] = tables(step);
             (void)kept;
             (void)st;
-            issue_exchange(ld, ld->plan().view(), step, mv, nm, off, ld->xpack[slot],
-                           ld->xrecv[slot], ld->side);
+            issue_exchange(ld, ld->plan().view(), step, mv, nm, off, regcnt(step),
+                           ld->xset[slot], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[slot], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
         }
         pend.valid = false;
-        pre = ld->xrecv[slot].as<uint8_t>();
+        pre = &ld->xset[slot];
     }
     // resize (K7): the prologue of this step was prefetched under the previous
     // step's augment, or runs now; that of the next step is issued after it
@@ -942,7 +1009,8 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
     }
     {
         auto [mv, off, kept, nm, st] = tables(step);
-        run_step(ld, epoch, ld->plan().view(), step, mv, off, kept, nm, st, info, pre, pslot);
+        run_step(ld, epoch, ld->plan().view(), step, mv, off, kept, nm, st, info, pre, pslot,
+                 regcnt(step));
     }
     if (rpre) {
         LL_CUDA(cudaEventRecord(ld->rdone[step & 1], ctx->stream));
@@ -979,8 +1047,8 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             auto [mv, off, kept, nm, st] = tables(step + 1);
             (void)kept;
             (void)st;
-            issue_exchange(ld, ld->plan().view(), step + 1, mv, nm, off, ld->xpack[ns],
-                           ld->xrecv[ns], ld->side);
+            issue_exchange(ld, ld->plan().view(), step + 1, mv, nm, off, regcnt(step + 1),
+                           ld->xset[ns], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[ns], ld->side));
             ld->xpending[ns] = {true, epoch, step + 1};
         }
@@ -1010,6 +1078,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             h.order.reserve(sizeof(uint32_t) * B);
             h.stage.reserve(sizeof(ll_loader::Tables) + sizeof(uint64_t) * B);
             h.plan.reserve(1, B);
+            if (reg_nccl(c)) h.plan.reserve_regcnt(1, p);
         }
         ensure_side_stream(ld);
     }
@@ -1071,12 +1140,19 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             k_stage<<<1, 256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), 0);
         });
         LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab, cudaMemcpyDeviceToHost, ctx->stream));
+        std::vector<uint32_t> rc;  // regular + NCCL: this step's [slice][owner] counts
+        if (pd.regcnt) {
+            rc.resize(static_cast<size_t>(p) * p);
+            LL_CUDA(cudaMemcpyAsync(rc.data(), pd.regcnt, sizeof(uint32_t) * rc.size(),
+                                    cudaMemcpyDeviceToHost, ctx->stream));
+        }
         LL_CUDA(cudaStreamSynchronize(ctx->stream));
         const auto* t = h.tab();
         ll_step_info local{};
-        run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local);
+        run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local, nullptr,
+                 -1, rc.empty() ? nullptr : rc.data());
         local.h2d_bytes = h.info.h2d_bytes;
-        local.d2h_bytes = tab;
+        local.d2h_bytes = tab + sizeof(uint32_t) * rc.size();
         h.info = local;
         h.n_local = local.n_local;
         launch(ctx, "stage", [&] {

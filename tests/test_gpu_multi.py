@@ -18,7 +18,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, exchange, dtype, out_dir):
+def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanced"):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
@@ -31,7 +31,7 @@ def _worker(rank, world, port, exchange, dtype, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     d, B, seed = 6000 * world, 192 * world, 42
     ld = DeviceLoader(LoaderConfig(d=d, learners=world, rank=rank, batch_size=B, seed=seed,
-                                   data_seed=seed, exchange=exchange,
+                                   data_seed=seed, exchange=exchange, scheme=scheme,
                                    augment=AugmentConfig(out_dtype=dtype)), device=rank)
     ld.populate()
     if exchange == "p2p":
@@ -48,7 +48,8 @@ def _worker(rank, world, port, exchange, dtype, out_dir):
     received = 0
     for t in [0, 1, 17, ld.steps_per_epoch - 1]:
         info = ld.step(1, t)
-        r = oracle.assign_step(order[t * B:(t + 1) * B], world, d, oracle.MODE_LOCALITY_BALANCED)
+        mode = (oracle.MODE_REGULAR if scheme == "regular" else oracle.MODE_LOCALITY_BALANCED)
+        r = oracle.assign_step(order[t * B:(t + 1) * B], world, d, mode)
         lst = r["final_ids"][r["final_off"][rank]:r["final_off"][rank + 1]]
         got_ids = ld.fetch_ids(info)
         if not np.array_equal(got_ids, lst):
@@ -79,12 +80,17 @@ def _n_gpus():
 
 
 @pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("exchange,dtype", [("nccl", "fp32"), ("p2p", "fp32"), ("p2p", "bf16")])
-def test_two_learners_exchange(tmp_path, exchange, dtype):
+@pytest.mark.parametrize("exchange,dtype,scheme", [
+    ("nccl", "fp32", "locality_balanced"), ("p2p", "fp32", "locality_balanced"),
+    ("p2p", "bf16", "locality_balanced"),
+    # reg_slice (sampling.cpp:27-42) at full volume: about half of every slice
+    # comes from the other learner
+    ("nccl", "bf16", "regular"), ("p2p", "fp32", "regular")])
+def test_two_learners_exchange(tmp_path, exchange, dtype, scheme):
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), exchange, dtype, str(tmp_path)), nprocs=world,
-             join=True)
+    mp.spawn(_worker, args=(world, _free_port(), exchange, dtype, str(tmp_path), scheme),
+             nprocs=world, join=True)
     total_recv = 0
     for r in range(world):
         lines = open(tmp_path / f"rank{r}.txt").read().splitlines()
