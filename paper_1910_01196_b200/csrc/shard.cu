@@ -101,32 +101,38 @@ __global__ void __launch_bounds__(1024) k_scan1(uint64_t* vals, uint64_t n) {
 
 // One CTA per owned sample: the generate_dataset bytes of sample first+t at
 // shard + prefix[first+t] - prefix[first], row y at y * var_pitch(w) (the
-// pitch padding is zero).  Thread per 32-bit word of the pitched rows; a word
-// spans at most two draws of the byte stream.
+// pitch padding is zero).  Thread per 16 bytes of a pitched row: they span at
+// most three 8-byte draws of the flat byte stream; four 32-bit stores (rows
+// are only word aligned).
 __global__ void __launch_bounds__(256) k_generate_var(uint8_t* __restrict__ shard, uint64_t first,
                                                       const uint64_t* __restrict__ prefix,
                                                       uint64_t data_seed) {
     const uint64_t id = first + blockIdx.x;
     uint32_t h, w;
     var_hw(data_seed, id, &h, &w);
-    const uint32_t row = 3 * w, words = var_pitch(w) / 4;
-    uint32_t* dst = reinterpret_cast<uint32_t*>(shard + (prefix[id] - prefix[first]));
+    const uint32_t row = 3 * w, pitch = var_pitch(w), q16 = (pitch + 15) / 16;
+    uint8_t* dst = shard + (prefix[id] - prefix[first]);
     const uint64_t key = derive_seed(data_seed, id);
-    for (uint32_t t = threadIdx.x; t < h * words; t += blockDim.x) {
-        const uint32_t y = t / words, q = t - y * words;
-        const uint32_t col = 4 * q;
-        uint32_t v = 0;
-        if (col < row) {
-            const uint64_t b0 = static_cast<uint64_t>(y) * row + col;  // flat byte index
-            const uint32_t sh = 8 * static_cast<uint32_t>(b0 & 7);
-            const uint64_t lo = draw_at(key, b0 >> 3);
-            uint64_t x = lo >> sh;
-            if (sh > 32) x |= draw_at(key, (b0 >> 3) + 1) << (64 - sh);
-            v = static_cast<uint32_t>(x);
-            const uint32_t valid = row - col;  // bytes of this word inside the row
-            if (valid < 4) v &= (1u << (8 * valid)) - 1;
+    for (uint32_t t = threadIdx.x; t < h * q16; t += blockDim.x) {
+        const uint32_t y = t / q16, col = 16 * (t - y * q16);
+        const uint64_t b0 = static_cast<uint64_t>(y) * row + col;  // flat byte index
+        const uint32_t sh = 8 * static_cast<uint32_t>(b0 & 7);
+        const uint64_t d0 = draw_at(key, b0 >> 3), d1 = draw_at(key, (b0 >> 3) + 1);
+        const uint64_t d2 = sh ? draw_at(key, (b0 >> 3) + 2) : 0;
+        // bytes b0 .. b0+15 as two 64-bit words
+        const uint64_t lo = sh ? (d0 >> sh) | (d1 << (64 - sh)) : d0;
+        const uint64_t hi = sh ? (d1 >> sh) | (d2 << (64 - sh)) : d1;
+        uint32_t* out = reinterpret_cast<uint32_t*>(dst + static_cast<uint64_t>(y) * pitch + col);
+        const uint32_t v[4] = {static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32),
+                               static_cast<uint32_t>(hi), static_cast<uint32_t>(hi >> 32)};
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+            const uint32_t c = col + 4 * i;
+            if (c >= pitch) break;
+            uint32_t x = v[i];
+            if (c + 4 > row) x = c >= row ? 0u : x & ((1u << (8 * (row - c))) - 1u);
+            out[i] = x;
         }
-        dst[t] = v;
     }
 }
 

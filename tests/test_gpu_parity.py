@@ -500,6 +500,53 @@ def test_loader_variable_size_resize_vs_oracle(dtype):
                 assert np.array_equal(got[k], want), (t, j, k, H, W)
 
 
+def test_loader_variable_size_consecutive_steps_prefetched_prologue():
+    """cfg5 over consecutive steps: from step 1 on, K7's prologue (per-sample
+    geometry and the pull of far windows from the peer's shard) was issued on
+    the side stream under the previous step's augment.  A host-path step in
+    between (its own buffer set) must not disturb the prefetched one."""
+    d, p, B, seed, epoch = 2400, 2, 64, 7, 1
+    lds = []
+    for j in range(p):
+        ld = DeviceLoader(LoaderConfig(d=d, height=0, width=0, learners=p, rank=j, batch_size=B,
+                                       seed=seed, data_seed=seed, exchange="p2p",
+                                       geometry="variable",
+                                       augment=AugmentConfig(mode="resize", out_dtype="bf16")))
+        ld.populate()
+        lds.append(ld)
+    DeviceLoader.link_peers(lds)
+    order = oracle.permute_epoch(seed, epoch, d)
+
+    def check(got, lst, kept):
+        ks = sorted(set(range(min(3, len(lst)))) | set(range(kept, len(lst))))
+        for k in ks:
+            sid = int(lst[k])
+            H, W = oracle.sample_hw(seed, sid)
+            src = oracle.gen_sample(seed, sid, H * W * 3).reshape(H, W, 3)
+            want = oracle.augment(src, sid, seed, epoch, mode=oracle.AUG_RESIZE, bf16=True)
+            assert np.array_equal(got[k], want), (k, sid, H, W)
+
+    far = 0
+    for t in range(6):
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, d, oracle.MODE_LOCALITY_BALANCED)
+        if t == 3:  # host path on learner 0 between two device-planned steps
+            ids = np.empty(B, np.uint64)
+            lds[0].submit_host(epoch, t, order[t * B:(t + 1) * B])
+            info = lds[0].wait_host(ids)
+            lst = r["final_ids"][r["final_off"][0]:r["final_off"][1]]
+            assert np.array_equal(ids[:info.n_local], lst)
+            check(lds[0].fetch(info), lst, info.kept)
+        for j, ld in enumerate(lds):
+            info = ld.step(epoch, t)
+            lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            check(ld.fetch(info), lst, info.kept)
+            far += len(lst) - info.kept
+    assert far > 0  # the steps really pulled windows from the peer
+    for ld in lds:
+        ld.close()
+
+
 def test_loader_host_submit_wait_pipelined():
     """Prefetching host API (prefetch_depth 2): in-order delivery, identical
     to the synchronous call and to the device-planned step."""
