@@ -586,6 +586,19 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
             s_base = it.src - phase;  // phase = 0 when ALIGNED
             s_q = it.q;
         }
+        // the band's source rows (crop span) head for L2 at once: one bulk
+        // prefetch per output row's lo and hi rows, issued before any tap
+        // (K7 138 -> 129 us: the L1 prefetch alone left most taps waiting on DRAM)
+        const uint8_t* rb = it.src + static_cast<uint64_t>(it.q.y0) * it.pitch + 3ull * it.q.x0;
+        for (uint32_t y : {ylo, yhi}) {
+            if (y == yhi && yhi == ylo) break;
+            const uintptr_t b = reinterpret_cast<uintptr_t>(rb + static_cast<uint64_t>(y) * it.pitch);
+            const uintptr_t s0 = b & ~static_cast<uintptr_t>(15);
+            const uintptr_t e16 = (b + 3ull * it.q.cw + 15) & ~static_cast<uintptr_t>(15);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s0),
+                         "r"(static_cast<uint32_t>(e16 - s0))
+                         : "memory");
+        }
     }
     __syncthreads();
     if (tid >= a.out_w) return;  // no barrier follows
@@ -730,13 +743,14 @@ static bool resize_banded(const ll_augment_spec& spec, const SrcMap& src, uint32
 }
 
 bool resize_prepare(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
-                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, int slot) {
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, int slot,
+                    const std::string& owner) {
     validate_spec(spec, height, width);
     uint64_t max_bytes = 0;
     if (spec.mode != LL_AUG_RESIZE || n == 0 || !resize_banded(spec, src, height, width, &max_bytes))
         return false;
     require(n < (1ull << 31), "augment: too many samples in one launch");
-    const std::string tag = std::to_string(slot);
+    const std::string tag = owner + std::to_string(slot);
     const AugArgs a = make_args(spec, seed, epoch, src, n, height, width, nullptr);
     DevBuf& items = ctx->buf("resize.items" + tag, sizeof(ResizeItem) * n);
     // far sources possible: peer shards (P2P) or the host storage tier
@@ -765,7 +779,7 @@ bool resize_prepare(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
 
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
                     const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out,
-                    int prepared_slot) {
+                    int prepared_slot, const std::string& owner) {
     validate_spec(spec, height, width);
     if (n == 0) return;
     const AugArgs a = make_args(spec, seed, epoch, src, n, height, width, d_out);
@@ -785,11 +799,13 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
         // the prologue (K7 prep + far pull) ran already (the loader prefetches
         // it on its side stream into sets 0/1) or runs now into set 2
         int slot = prepared_slot;
-        if (slot < 0) {
-            resize_prepare(ctx, spec, seed, epoch, src, n, height, width, 2);
+        std::string who = owner;
+        if (slot < 0) {  // inline: on the context stream, so one set serves every caller
+            who.clear();
+            resize_prepare(ctx, spec, seed, epoch, src, n, height, width, 2, who);
             slot = 2;
         }
-        const ResizeItem* it = ctx->buf("resize.items" + std::to_string(slot),
+        const ResizeItem* it = ctx->buf("resize.items" + who + std::to_string(slot),
                                         sizeof(ResizeItem) * n).as<ResizeItem>();
         const dim3 grid(static_cast<unsigned>(n), (spec.out_h + kRB - 1) / kRB);
         const unsigned threads = 32 * ((spec.out_w + 31) / 32);

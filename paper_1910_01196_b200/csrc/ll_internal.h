@@ -215,14 +215,18 @@ struct SrcMap {
     // regular scheme over NCCL: list position -> recv index (0xFFFFFFFF: own shard)
     const uint32_t* recv_idx = nullptr;
 };
-// prepared_slot >= 0: the resize prologue already ran into that buffer set
+// prepared_slot >= 0: the resize prologue already ran into buffer set
+// (owner, prepared_slot)
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
                     const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, void* d_out,
-                    int prepared_slot = -1);
+                    int prepared_slot = -1, const std::string& owner = std::string());
 // Resize prologue (per-sample geometry, far-sample pull) into buffer set
-// `slot` on ctx->stream; false when the step has no banded-resize prologue.
+// (owner, slot) on ctx->stream; false when the step has no banded-resize
+// prologue.  Work on a stream other than the context's needs an owner name
+// of its own: loaders sharing a device share its context and scratch.
 bool resize_prepare(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
-                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, int slot);
+                    const SrcMap& src, uint64_t n, uint32_t height, uint32_t width, int slot,
+                    const std::string& owner = std::string());
 void augment_params_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed,
                            uint64_t epoch, const uint64_t* d_ids, uint64_t n, uint32_t height,
                            uint32_t width, uint32_t* d_params5);

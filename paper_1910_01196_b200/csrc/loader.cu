@@ -43,6 +43,9 @@ void widen_device(ll_ctx* ctx, const uint32_t* in, uint64_t* out, uint64_t n);
 
 struct ll_loader {
     ll_ctx* ctx = nullptr;
+    // names this loader's context scratch that its own streams (plan, side)
+    // write: loaders on one device share the context
+    std::string tag;
     ll_loader_config cfg{};
     uint64_t S = 0;               // sample bytes
     uint64_t cached = 0;          // CacheDirectory::cached_count
@@ -168,12 +171,12 @@ void plan_into(ll_loader* ld, int k, uint64_t epoch, cudaStream_t stream) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     auto& sl = ld->slot[k];
-    const char* tag = k ? "plan1" : "plan0";
+    const std::string tag = ld->tag + (k ? ".plan1" : ".plan0");
     cudaStream_t main = ctx->stream;
     ctx->stream = stream;  // the device helpers launch on the context stream
     try {
         permute_device(ctx, c.seed, epoch, static_cast<uint32_t>(c.d), sl.order.as<uint32_t>(),
-                       nullptr, 0, tag);
+                       nullptr, 0, tag.c_str());
         assign_device(ctx, sl.order.as<uint32_t>(), ld->steps, c.batch_size, c.learners,
                       ld->cached, c.scheme, sl.plan.view(), aug_plan(ld, epoch));
         copy_tables(ld, k, stream);
@@ -383,7 +386,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     void* out = ld->out[ld->out_slot]->ptr;
     ld->out_slot = (ld->out_slot + 1) % ld->out.size();
     augment_device(ctx, c.augment, c.seed, epoch, src, n_local, geom_h(c), geom_w(c), out,
-                   prepared_slot);
+                   prepared_slot, ld->tag);
     if (info) {
         info->epoch = epoch;
         info->step = step;
@@ -486,6 +489,8 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
         require(c.batch_size % c.learners == 0,
                 "reg_slice: learner count must divide the batch size");
     auto ld = std::make_unique<ll_loader>();
+    static std::atomic<uint64_t> serial{0};
+    ld->tag = "ld" + std::to_string(serial++);
     ld->ctx = ctx;
     ld->cfg = c;
     require(c.geometry == LL_GEOM_FIXED || c.geometry == LL_GEOM_VARIABLE,
@@ -879,7 +884,7 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
         LL_CUDA(cudaStreamWaitEvent(ctx->stream, sl.ready, 0));  // prefetched
     }
     LL_CUDA(cudaEventSynchronize(sl.ready));
-    permute_rounds(ctx, k ? "plan1" : "plan0");  // raises if the round guard tripped
+    permute_rounds(ctx, (ld->tag + (k ? ".plan1" : ".plan0")).c_str());  // raises if the round guard tripped
     ld->cur = k;
     ld->h_moves = sl.moves;
     ld->h_off = sl.off;
@@ -1002,7 +1007,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             (void)st;
             const StepSrc ss = step_src(ld, ld->plan().view(), step, mv, off, kept, nm);
             if (resize_prepare(ctx, c.augment, c.seed, epoch, ss.src, ss.n_local, geom_h(c),
-                               geom_w(c), rs))
+                               geom_w(c), rs, ld->tag))
                 pslot = rs;
         }
         rp.valid = false;
@@ -1026,7 +1031,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             bool ok = false;
             try {
                 ok = resize_prepare(ctx, c.augment, c.seed, epoch, ss.src, ss.n_local, geom_h(c),
-                                    geom_w(c), ns);
+                                    geom_w(c), ns, ld->tag);
             } catch (...) {
                 ctx->stream = main;
                 throw;
