@@ -492,16 +492,15 @@ __device__ __forceinline__ void st_cs_u16(void* p, uint16_t v) {
 
 // K7 banded: one CTA per (sample, kRB output rows), one thread per output
 // column, walking the band two rows at a time (the pair is one fp32x2).  The
-// taps are 32-bit read-only loads straight from the source rows, which stay
-// L1-resident while the band is in flight; each iteration prefetches the rows
-// of the pair kPrefetchAhead rows below into L1.  No shared-memory staging:
+// taps are 32-bit read-only loads straight from the source rows; at CTA start
+// the band's source rows are bulk-prefetched into L2 (a per-iteration L1
+// prefetch on top of that measured slower, profiles/r05_k7_ab.md).  No shared-memory staging:
 // occupancy is not bound by the largest (512 px) source, and the A/B against
 // a staged-smem band kernel (profiles/r03_k7_ab.md) favoured the gathers.
 // Only words holding needed bytes are read: a far-edge column (wx = 0) taps
 // pixels (xlo-1, xlo) with weights (0, 128), and the third word is loaded
 // only when tap b spills into it.
 constexpr uint32_t kRB = 16;
-constexpr uint32_t kPrefetchAhead = 4;
 __device__ __forceinline__ void row_taps_g(const uint8_t* base, uint32_t off, uint32_t* rg,
                                            uint32_t* bb) {
     const uint32_t* p = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
@@ -545,10 +544,6 @@ __device__ __forceinline__ void bilerp_a(const uint8_t* colp, uint32_t sel, uint
     v[0] = __dp2a_lo(w0, rg0, __dp2a_lo(w1, rg1, 0u));
     v[1] = __dp2a_hi(w0, rg0, __dp2a_hi(w1, rg1, 0u));
     v[2] = __dp2a_lo(w0, b0, __dp2a_lo(w1, b1, 0u));
-}
-
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
 
 // ALIGNED (word-aligned rows and sample starts): the row table holds the row
@@ -657,12 +652,6 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
     uint32_t rr = 0;
     for (; rr + 1 < rows_out; rr += 2) {
         uint32_t v0[3], v1[3];
-        if (rr + kPrefetchAhead < rows_out) {
-            // pull the source rows of a later row pair into L1 while this one computes
-            const uint4 f = s_row[rr + kPrefetchAhead];
-            prefetch_l1((ALIGNED ? colp : base + x3) + f.x);
-            prefetch_l1((ALIGNED ? colp : base + x3) + f.y);
-        }
         bilerp(s_row[rr], v0);
         bilerp(s_row[rr + 1], v1);
         emit(v0, v1, true);
