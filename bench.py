@@ -36,7 +36,6 @@ H = W = 256
 CROP = 224
 SEED = 42
 SRC_BYTES = CROP * CROP * 3                    # crop window read per sample
-PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "augment_crop_traffic.json")
 
 
 def out_bytes(dtype: str) -> int:
@@ -412,7 +411,7 @@ def run_ours(args):
         peak, peak_src = 6650.0, "B200_PROFILING.md fallback"
     traffic = None
     try:
-        with open(PROFILE_SUMMARY) as f:
+        with open(os.path.join(ROOT, "profiles", f"{aug_kernel}_traffic.json")) as f:
             prof = json.load(f)
         if (prof.get("dtype") == args.dtype and prof.get("per_gpu_batch") == args.per_gpu_batch
                 and prof.get("kernel") == aug_kernel):

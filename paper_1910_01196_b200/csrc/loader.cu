@@ -120,6 +120,8 @@ struct ll_loader {
         ll_step_info info{};
         uint64_t n_local = 0;
         bool synchronous = false;
+        std::string rtag;                // owner name of this slot's K7 prologue set
+        int rslot = -1;                  // K7 prologue prepared into (rtag, 0), or -1
         Tables* tab() const { return reinterpret_cast<Tables*>(pin); }
         uint64_t* ids() const { return pin + sizeof(Tables) / 8; }
     };
@@ -171,7 +173,7 @@ void plan_into(ll_loader* ld, int k, uint64_t epoch, cudaStream_t stream) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     auto& sl = ld->slot[k];
-    const std::string tag = ld->tag + (k ? ".plan1" : ".plan0");
+    const std::string tag = ld->tag + (k ? "plan1" : "plan0");
     cudaStream_t main = ctx->stream;
     ctx->stream = stream;  // the device helpers launch on the context stream
     try {
@@ -405,8 +407,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
 // A step whose plan tables stay on the device (host-driven path): the list
 // offset and kept count are read by the kernel, n_local is the balanced
 // target (or the regular slice), so no mid-step host sync is needed.
-void* run_step_devplan(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t n_local) {
-    ll_ctx* ctx = ld->ctx;
+SrcMap devplan_src(ll_loader* ld, const PlanDev& pd) {
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
     SrcMap src;
@@ -433,12 +434,20 @@ void* run_step_devplan(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_
             src.kept = 0;
         }
     }
+    return src;
+}
+
+// prepared_slot >= 0: the resize prologue ran into set (owner, prepared_slot)
+void* run_step_devplan(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t n_local,
+                       int prepared_slot = -1, const std::string& owner = std::string()) {
+    ll_ctx* ctx = ld->ctx;
+    const ll_loader_config& c = ld->cfg;
+    const SrcMap src = devplan_src(ld, pd);
     ensure_out(ld);
     void* out = ld->out[ld->out_slot]->ptr;
     ld->out_slot = (ld->out_slot + 1) % ld->out.size();
-    const uint32_t gh = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.height;
-    const uint32_t gw = c.geometry == LL_GEOM_VARIABLE ? kVarMin + kVarSpan - 1 : c.width;
-    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, gh, gw, out);
+    augment_device(ctx, c.augment, c.seed, epoch, src, n_local, geom_h(c), geom_w(c), out,
+                   prepared_slot, owner);
     return out;
 }
 
@@ -490,7 +499,7 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
                 "reg_slice: learner count must divide the batch size");
     auto ld = std::make_unique<ll_loader>();
     static std::atomic<uint64_t> serial{0};
-    ld->tag = "ld" + std::to_string(serial++);
+    ld->tag = "ld" + std::to_string(serial++) + ".";
     ld->ctx = ctx;
     ld->cfg = c;
     require(c.geometry == LL_GEOM_FIXED || c.geometry == LL_GEOM_VARIABLE,
@@ -884,7 +893,7 @@ void loader_plan_epoch(ll_loader* ld, uint64_t epoch) {
         LL_CUDA(cudaStreamWaitEvent(ctx->stream, sl.ready, 0));  // prefetched
     }
     LL_CUDA(cudaEventSynchronize(sl.ready));
-    permute_rounds(ctx, (ld->tag + (k ? ".plan1" : ".plan0")).c_str());  // raises if the round guard tripped
+    permute_rounds(ctx, (ld->tag + (k ? "plan1" : "plan0")).c_str());  // raises if the round guard tripped
     ld->cur = k;
     ld->h_moves = sl.moves;
     ld->h_off = sl.off;
@@ -1071,7 +1080,10 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     require(ld->submitted - ld->waited < F,
             "Loader: prefetch_depth host steps already outstanding (wait first)");
     if (ld->hslots.empty()) {
-        for (uint32_t f = 0; f < F; ++f) ld->hslots.emplace_back(new ll_loader::HostSlot());
+        for (uint32_t f = 0; f < F; ++f) {
+            ld->hslots.emplace_back(new ll_loader::HostSlot());
+            ld->hslots.back()->rtag = ld->tag + "h" + std::to_string(f) + ".";
+        }
         for (auto& hp : ld->hslots) {
             auto& h = *hp;
             LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h.pin),
@@ -1089,6 +1101,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     }
     auto& h = *ld->hslots[ld->submitted % F];
     h.info = ll_step_info{};
+    h.rslot = -1;
     h.info.epoch = epoch;
     h.info.step = step;
     std::memcpy(h.pin_batch, host_batch, sizeof(uint64_t) * B);
@@ -1112,6 +1125,13 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
         narrow_device(ctx, h.batch64.as<uint64_t>(), h.order.as<uint32_t>(), B);
         assign_device(ctx, h.order.as<uint32_t>(), 1, B, p, ld->cached, c.scheme, pd,
                       aug_plan(ld, epoch));
+        if (devplan && c.augment.mode == LL_AUG_RESIZE) {
+            // K7's prologue (geometry, far pulls, row table) too: it needs the plan only
+            h.rslot = resize_prepare(ctx, c.augment, c.seed, epoch, devplan_src(ld, pd),
+                                     h.n_local, geom_h(c), geom_w(c), 0, h.rtag)
+                          ? 0
+                          : -1;
+        }
         if (devplan) {
             // the step's tables and local ids back to the host, also under the
             // previous step's augment (they depend on the plan only)
@@ -1135,7 +1155,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     if (devplan) {
         // fully asynchronous: the kernel reads the list offset and kept count
         // from the device plan
-        void* out = run_step_devplan(ld, epoch, pd, h.n_local);
+        void* out = run_step_devplan(ld, epoch, pd, h.n_local, h.rslot, h.rtag);
         h.info.d2h_bytes = tab + sizeof(uint64_t) * h.n_local;
         h.info.device_out = reinterpret_cast<uintptr_t>(out);
     } else {

@@ -94,19 +94,26 @@ def main():
                 vals.append(f"{r[i]} {units[i]}".strip())
             name = r[ki].split("(")[0].replace("(anonymous namespace)::", "")
             md.append(f"| `{name}` | " + " | ".join(vals) + " |")
-            if "augment_crop" in name:
+            kern = ("augment_crop" if "augment_crop" in name else
+                    "augment_resize" if "augment_resize" in name else None)
+            if kern:
                 rd = to_bytes(float(r[hdr.index("dram__bytes_read.sum")]), units[hdr.index("dram__bytes_read.sum")])
                 wr = to_bytes(float(r[hdr.index("dram__bytes_write.sum")]), units[hdr.index("dram__bytes_write.sum")])
                 grid = int(float(r[hdr.index("launch__grid_size")]))
-                aug.append((rd, wr, grid, "<1>" in r[ki] or "<true>" in r[ki]))
+                bf16 = r[ki].split("<")[1].startswith(("1", "true")) if "<" in r[ki] else False
+                aug.append((rd, wr, grid, bf16, kern))
         md.append("")
         if aug:
-            rd = sum(a[0] for a in aug) / len(aug)
-            wr = sum(a[1] for a in aug) / len(aug)
-            traffic = {"kernel": "augment_crop", "tag": tag, "dram_read_bytes_per_launch": rd,
+            kern = aug[0][4]
+            sel = [a for a in aug if a[4] == kern]
+            rd = sum(a[0] for a in sel) / len(sel)
+            wr = sum(a[1] for a in sel) / len(sel)
+            # crop: 7 bands per sample; resize: 14 bands of 16 rows per sample (224 out)
+            per = 7 if kern == "augment_crop" else 14
+            traffic = {"kernel": kern, "tag": tag, "dram_read_bytes_per_launch": rd,
                        "dram_write_bytes_per_launch": wr, "dram_bytes_per_launch": rd + wr,
-                       "grid": aug[0][2], "dtype": "bf16" if aug[0][3] else "fp32",
-                       "per_gpu_batch": aug[0][2] // 7 if aug[0][2] % 7 == 0 else None,
+                       "grid": sel[0][2], "dtype": "bf16" if sel[0][3] else "fp32",
+                       "per_gpu_batch": sel[0][2] // per if sel[0][2] % per == 0 else None,
                        "note": "writes still dirty in L2 at kernel end are not counted"}
     out_md = os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md")
     os.makedirs(os.path.dirname(out_md), exist_ok=True)
@@ -114,7 +121,7 @@ def main():
         f.write("\n".join(md) + "\n")
     print(out_md)
     if traffic:
-        p = os.path.join(ROOT, "profiles", "augment_crop_traffic.json")
+        p = os.path.join(ROOT, "profiles", f"{traffic['kernel']}_traffic.json")
         with open(p, "w") as f:
             json.dump(traffic, f, indent=1)
         print(p, traffic)
