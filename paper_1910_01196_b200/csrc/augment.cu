@@ -581,24 +581,29 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
             s_base = it.src - phase;  // phase = 0 when ALIGNED
             s_q = it.q;
         }
-        // the band's source rows (crop span) head for L2 at once: one bulk
-        // prefetch per output row's lo and hi rows, issued before any tap
-        // (K7 138 -> 129 us: the L1 prefetch alone left most taps waiting on DRAM)
-        const uint8_t* rb = it.src + static_cast<uint64_t>(it.q.y0) * it.pitch + 3ull * it.q.x0;
-        for (uint32_t y : {ylo, yhi}) {
-            if (y == yhi && yhi == ylo) break;
-            const uintptr_t b = reinterpret_cast<uintptr_t>(rb + static_cast<uint64_t>(y) * it.pitch);
-            const uintptr_t s0 = b & ~static_cast<uintptr_t>(15);
-            const uintptr_t e16 = (b + 3ull * it.q.cw + 15) & ~static_cast<uintptr_t>(15);
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s0),
-                         "r"(static_cast<uint32_t>(e16 - s0))
-                         : "memory");
-        }
     }
     __syncthreads();
-    if (tid >= a.out_w) return;  // no barrier follows
     const Params q = s_q;
     const uint8_t* base = s_base;
+    {
+        // the band's source rows (crop span) head for L2 at once: every
+        // thread prefetches about two 128-byte lines of the band's lo / hi
+        // rows before any tap (K7 138 -> 123 us; per-thread line prefetches,
+        // as the bulk prefetch takes uniform operands and serialises)
+        const uint32_t lines = (3 * q.cw + 127) / 128 + 1;  // per row span, any alignment
+        const uint32_t total = 2 * rows_out * lines;
+        const uint32_t xo = ALIGNED ? 3 * q.x0 : 0;
+        for (uint32_t j = tid; j < total; j += blockDim.x) {
+            const uint32_t r = j / (2 * lines), t = j - r * 2 * lines;
+            const uint4 e = s_row[r];
+            if (t >= lines && e.w == 0) continue;  // wy = 0: no hi row
+            const uint32_t l = t < lines ? t : t - lines;
+            const uint32_t in = 128 * l < 3 * q.cw ? 128 * l : 3 * q.cw - 1;  // stay in the span
+            const uint32_t off = (t < lines ? e.x : e.y) + xo + in;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + off));
+        }
+    }
+    if (tid >= a.out_w) return;  // no barrier follows
     const uint32_t ox = tid;
     uint32_t xlo, wx;
     resize_tap<uint32_t>(q.flip ? a.out_w - 1 - ox : ox, a.out_w, q.cw, &xlo, &wx);
