@@ -274,9 +274,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
         s_k = k;
         uint64_t id;
         const uint8_t* src;
-        resolve(a.src, k, &id, &src);
+        bool far = false;
+        resolve(a.src, k, &id, &src, &far);
         s_src = src;
+#ifdef LL_K6_TMA_FAR
+        s_host = far;
+#else
         s_host = a.src.kind == 1 && a.src.storage && !a.src.recv_idx && id >= a.src.cached;
+#endif
         if (s_host) {  // the band comes by TMA (below); waited on after the barrier
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
                              static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar)))
