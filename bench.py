@@ -135,7 +135,9 @@ def workload(args, n):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """NVML (the library nvidia-smi reads) polled every ~2 ms in a thread."""
+    """NVML (the library nvidia-smi reads) polled every ~20 ms in a thread.
+    (At 2 ms the NVML calls contended with the CUDA/NCCL calls of the step
+    loop for the driver: NCCL-exchange runs at N = 2 lost up to 2x.)"""
     NAMES = {0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
              0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
              0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
@@ -167,7 +169,7 @@ class ClockSampler:
                 self.samples.append((mhz, rs, mem))
             except Exception:
                 pass
-            time.sleep(0.002)
+            self._stop.wait(0.02)
 
     def __enter__(self):
         if self.ok:
