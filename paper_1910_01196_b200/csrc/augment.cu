@@ -703,97 +703,6 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
     }
 }
 
-#ifdef LL_K7_COLS2
-// K7, two adjacent output columns per thread (word-aligned rows, 224 x 224):
-// one CTA = one sample x 32 output rows as two groups of 16; thread t of
-// group g = t / 112 owns columns (2u, 2u+1), u = t % 112, so 224 threads are
-// 7 full warps.  Per row the two columns' values form the fp32x2 of the
-// normalisation and leave as one bf16x2 / fp32x2 store per plane.
-template <bool BF16>
-__global__ void __launch_bounds__(224) k_augment_resize_c2(AugArgs a, const ResizeItem* items) {
-    constexpr uint32_t OUT = 224, RB = 2 * kRB;
-    __shared__ uint4 s_row[RB];
-    __shared__ const uint8_t* s_base;
-    __shared__ Params s_q;
-    const uint64_t k = blockIdx.x;
-    const uint32_t oy0 = blockIdx.y * RB;
-    const uint32_t tid = threadIdx.x;
-    if (tid < RB) {
-        const ResizeItem it = items[k];
-        uint32_t ylo, wy;
-        resize_tap<uint32_t>(oy0 + tid, OUT, it.q.ch, &ylo, &wy);
-        const uint32_t yhi = wy ? ylo + 1 : ylo;
-        s_row[tid] = make_uint4((it.q.y0 + ylo) * it.pitch, (it.q.y0 + yhi) * it.pitch, 128 - wy, wy);
-        if (tid == 0) {
-            s_base = it.src;
-            s_q = it.q;
-        }
-    }
-    __syncthreads();
-    const Params q = s_q;
-    const uint8_t* base = s_base;
-    {
-        const uint32_t lines = (3 * q.cw + 127) / 128 + 1;
-        const uint32_t total = 2 * RB * lines;
-        for (uint32_t j = tid; j < total; j += blockDim.x) {
-            const uint32_t r = j / (2 * lines), t = j - r * 2 * lines;
-            const uint4 e = s_row[r];
-            if (t >= lines && e.w == 0) continue;
-            const uint32_t l = t < lines ? t : t - lines;
-            const uint32_t in = 128 * l < 3 * q.cw ? 128 * l : 3 * q.cw - 1;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(base + (t < lines ? e.x : e.y) + 3 * q.x0 + in));
-        }
-    }
-    const uint32_t g = tid / (OUT / 2), u = tid - g * (OUT / 2);
-    const uint32_t ox = 2 * u;
-    uint32_t sel[2], colw[2];
-    const uint8_t* colp[2];
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-        uint32_t xlo, wx;
-        resize_tap<uint32_t>(q.flip ? OUT - 1 - (ox + c) : ox + c, OUT, q.cw, &xlo, &wx);
-        uint32_t x3 = 3 * xlo;
-        colw[c] = (128 - wx) | (wx << 16);
-        if (wx == 0 && xlo > 0) {
-            x3 -= 3;
-            colw[c] = 128u << 16;
-        }
-        const uint32_t xb = 3 * q.x0 + x3;
-        colp[c] = base + (xb & ~3u);
-        sel[c] = xb & 3u;
-    }
-    uint64_t mean2[3], inv2[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        mean2[c] = pk(__float_as_uint(a.nc.mean255[c]), __float_as_uint(a.nc.mean255[c]));
-        inv2[c] = pk(__float_as_uint(a.nc.inv_std255[c]), __float_as_uint(a.nc.inv_std255[c]));
-    }
-    const uint64_t k512 = 0x4400000044000000ull;
-    constexpr uint64_t plane = static_cast<uint64_t>(OUT) * OUT;
-    const uint64_t o0 = k * 3 * plane + static_cast<uint64_t>(oy0 + g * kRB) * OUT + ox;
-#pragma unroll 1
-    for (uint32_t rr = 0; rr < kRB; ++rr) {
-        const uint4 r = s_row[g * kRB + rr];
-        uint32_t v0[3], v1[3];
-        bilerp_a(colp[0], sel[0], colw[0], r, v0);
-        bilerp_a(colp[1], sel[1], colw[1], r, v1);
-        const uint64_t o = o0 + static_cast<uint64_t>(rr) * OUT;
-#pragma unroll
-        for (uint32_t c = 0; c < 3; ++c) {
-            const uint64_t m = pk(0x44000000u | v0[c], 0x44000000u | v1[c]);
-            const uint64_t f = mul2(sub2(sub2(m, k512), mean2[c]), inv2[c]);
-            if constexpr (BF16) {
-                asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(static_cast<uint16_t*>(a.out) + o + c * plane),
-                             "r"(bf16x2(f)) : "memory");
-            } else {
-                asm volatile("st.global.cs.v2.u32 [%0], {%1, %2};" ::"l"(static_cast<float*>(a.out) + o + c * plane),
-                             "r"(lo32(f)), "r"(hi32(f)) : "memory");
-            }
-        }
-    }
-}
-#endif
-
 __global__ void k_aug_params(uint64_t seed, uint64_t epoch, const uint64_t* __restrict__ ids,
                              uint64_t n, uint32_t H, uint32_t W, uint32_t out_h, uint32_t out_w,
                              int mode, uint32_t* __restrict__ out5) {
@@ -932,18 +841,6 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
         // word-aligned rows: the variable-geometry shard layout (geometry.cuh)
         const bool aligned = src.prefix != nullptr;
         const bool out224 = spec.out_h == 224 && spec.out_w == 224;
-#ifdef LL_K7_COLS2
-        if (aligned && out224) {
-            launch(ctx, "augment_resize", [&] {
-                const dim3 g2(static_cast<unsigned>(n), 224 / (2 * kRB));
-                if (bf16)
-                    k_augment_resize_c2<true><<<g2, 224, 0, ctx->stream>>>(a, it);
-                else
-                    k_augment_resize_c2<false><<<g2, 224, 0, ctx->stream>>>(a, it);
-            });
-            return;
-        }
-#endif
         launch(ctx, "augment_resize", [&] {
             if (bf16 && aligned && out224)
                 k_augment_resize_rows<true, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
