@@ -97,3 +97,22 @@ def test_two_learners_exchange(tmp_path, exchange, dtype, scheme):
         total_recv += int(lines[0].split()[1])
         assert lines[1:] == [], lines[1:]
     assert total_recv > 0  # the steps really exercised the exchange
+
+
+@pytest.mark.skipif(_n_gpus() < 4, reason="needs >= 4 GPUs")
+@pytest.mark.parametrize("exchange,scheme", [("p2p", "locality_balanced"),
+                                             ("nccl", "locality_balanced"),
+                                             ("nccl", "regular")])
+def test_four_learners_exchange(tmp_path, exchange, scheme):
+    """The same checks with four learners: moves between several peer pairs
+    per step, every learner's batch against the oracle."""
+    import torch.multiprocessing as mp
+    world = 4
+    mp.spawn(_worker, args=(world, _free_port(), exchange, "bf16", str(tmp_path), scheme),
+             nprocs=world, join=True)
+    total_recv = 0
+    for r in range(world):
+        lines = open(tmp_path / f"rank{r}.txt").read().splitlines()
+        total_recv += int(lines[0].split()[1])
+        assert lines[1:] == [], lines[1:]
+    assert total_recv > 0
