@@ -433,6 +433,9 @@ def run_ours(args):
         for s_ in range(min(args.warmup, spe)):
             ld.submit_host(0, s_, wo[s_ * B:(s_ + 1) * B])
             ld.wait_host(pinned_ids)
+        from paper_1910_01196_b200.locload import context
+        perm_ctx = context(local)
+        perm_pinned = torch.empty(d, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
         barrier()
         t0 = time.perf_counter()
         e_cur = None
@@ -441,7 +444,10 @@ def run_ours(args):
         for t in range(start, start + k_e2e):
             e, s = divmod(t, spe)
             if e != e_cur:
-                order = ll.permute_epoch(SEED, e, d, device=local).order  # device plan, D2H
+                # epoch order computed on the device, D2H into pinned host memory
+                _capi.check(lib.ll_permute_epoch(perm_ctx, SEED, e, d,
+                                                 perm_pinned.ctypes.data_as(C.POINTER(C.c_uint64))))
+                order = perm_pinned
                 d2h += 8 * d
                 e_cur = e
             ld.submit_host(e, s, order[s * B:(s + 1) * B])  # GlobalBatch from host memory
