@@ -13,9 +13,15 @@
 // 224x224x3 window (150,528 B) and writes 602,112 B (fp32) or 301,056 B
 // (bf16).  One CTA = one sample x one 32-row band.  The band's source rows
 // (the crop window widened to 16-byte alignment, <= 688 B per row) are pulled
-// into shared memory with 128-bit non-allocating loads; each thread then emits
-// PX consecutive output pixels of all three planes as 128-bit streaming
-// stores, so every warp writes 512 contiguous bytes per plane row.
+// into shared memory with 128-bit non-allocating loads (far samples -- peer
+// shards, host storage -- by TMA bulk copies); each thread then emits PX
+// consecutive output pixels of all three planes as 128-bit streaming stores,
+// so every warp writes 512 contiguous bytes per plane row.
+//
+// K7 (cfg5, variable-size sources, bilinear resize to 224): one CTA per
+// (sample, 16 output rows), one output column per thread; taps from
+// word-aligned source rows (geometry.cuh var_pitch) with the band's rows
+// prefetched into L2; see the K7 section below and DESIGN.md section 5.
 #include "ll_internal.h"
 #include "geometry.cuh"
 #include "locload_rng.cuh"
