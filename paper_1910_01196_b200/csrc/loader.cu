@@ -599,6 +599,19 @@ void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     std::memcpy(&id, id128, sizeof(id));
     LL_NCCL(ncclCommInitRank(&ld->comm, static_cast<int>(ld->cfg.learners), id,
                              static_cast<int>(ld->cfg.rank)));
+    // Every exchange buffer at its largest size now: a buffer grown on the step
+    // path is a cudaFree + cudaMalloc, which synchronises the device while peer
+    // ranks' NCCL kernels wait on this rank's next send/recv -- a deadlock.
+    // Sends are at most the batch, receives at most this learner's share.
+    const ll_loader_config& c = ld->cfg;
+    const uint64_t B = c.batch_size, p = c.learners;
+    const uint64_t share = (B + p - 1) / p;
+    for (ll_loader::ExSet* x : {&ld->xcur, &ld->xset[0], &ld->xset[1]}) {
+        x->pack.reserve(std::max<uint64_t>(B * ld->S, 16));
+        x->recv.reserve(std::max<uint64_t>((c.scheme == LL_SCHEME_REGULAR ? B : share) * ld->S, 16));
+        x->ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(share, 1));
+    }
+    LL_CUDA(cudaDeviceSynchronize());
 }
 
 void loader_ipc_handle(ll_loader* ld, uint8_t* out64) {
