@@ -71,8 +71,11 @@ __device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
 // *far (optional): the bytes live outside this GPU's HBM (a peer shard over
 // NVLink, or the host storage tier over PCIe).
 __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* id,
-                                        const uint8_t** src, bool* far = nullptr) {
+                                        const uint8_t** src, bool* far = nullptr,
+                                        bool* win = nullptr) {  // *win: src is a window slot
     if (far) *far = false;
+    if (win) *win = false;
+    const uint64_t slot = m.recv_row ? kWinBytes : m.sample_bytes;
     if (m.kind == 0) {
         *id = m.ids[k];
         *src = m.base + k * m.sample_bytes;
@@ -87,7 +90,8 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
         if (ri == 0xFFFFFFFFu) {
             *src = m.shard + (s - m.shard_first) * m.sample_bytes;
         } else {
-            *src = m.recv + static_cast<uint64_t>(ri) * m.sample_bytes;
+            *src = m.recv + static_cast<uint64_t>(ri) * slot;
+            if (win) *win = m.recv_row != 0;
         }
         return;
     }
@@ -104,7 +108,8 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
         *src = m.peers[o] + (m.prefix ? m.prefix[s] - m.prefix[first] : (s - first) * m.sample_bytes);
         if (far) *far = true;
     } else {
-        *src = m.recv + (k - kept) * m.sample_bytes;
+        *src = m.recv + (k - kept) * slot;
+        if (win) *win = m.recv_row != 0;
     }
 }
 
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     __shared__ Params s_prm;
     __shared__ uint64_t s_k;
     __shared__ __align__(8) uint64_t s_mbar;
-    __shared__ uint32_t s_host;
+    __shared__ uint32_t s_host, s_win;
 
     const uint64_t kb = blockIdx.x / kBands;
     const uint32_t band = blockIdx.x - static_cast<uint32_t>(kb) * kBands;
@@ -280,9 +285,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
         s_k = k;
         uint64_t id;
         const uint8_t* src;
-        bool far = false;
-        resolve(a.src, k, &id, &src, &far);
+        bool far = false, win = false;
+        resolve(a.src, k, &id, &src, &far, &win);
         s_src = src;
+        s_win = win;
         s_host = far;  // peer shard (NVLink) or host storage tier (PCIe)
         if (s_host) {  // the band comes by TMA (below); waited on after the barrier
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
@@ -302,10 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     const Params q = s_prm;
     const uint8_t* src = s_src;
     const uint64_t k = s_k;
-    const uint32_t row_bytes = a.W * 3;
+    // a received crop window (NCCL slot) holds exactly the spans read below
+    const bool win = s_win != 0;
+    const uint32_t row_bytes = win ? kWinRow : a.W * 3;
     const uint32_t a0 = (3 * q.x0) & ~15u;
     const uint32_t nch = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
-    const uint8_t* gbase = src + static_cast<uint64_t>(q.y0 + band * kBand) * row_bytes + a0;
+    const uint8_t* gbase = win ? src + static_cast<uint64_t>(band * kBand) * kWinRow
+                               : src + static_cast<uint64_t>(q.y0 + band * kBand) * row_bytes + a0;
     if (s_host) {
         // far samples (host storage tier, peer shards): the band's 32 row
         // segments as TMA bulk copies instead of 16-byte loads (cfg3: 0.78 ->

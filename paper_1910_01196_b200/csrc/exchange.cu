@@ -16,6 +16,31 @@ namespace {
 
 constexpr uint32_t kChunk = 16384;
 
+// One sample into a message slot: the whole sample, or (win) its crop
+// window's 224 rows as the 16-byte-aligned spans K6 reads, at kWinRow pitch
+// (157,696 B instead of 196,608 B on the wire).  CTA part of parts.
+__device__ __forceinline__ void copy_slot(const uint8_t* src, uint8_t* dst, uint64_t sample_bytes,
+                                          bool win, uint32_t crop, uint32_t row_bytes,
+                                          uint32_t part, uint32_t parts) {
+    if (!win) {
+        const uint64_t n16 = sample_bytes / 16;
+        for (uint64_t c = part * blockDim.x + threadIdx.x; c < n16;
+             c += static_cast<uint64_t>(parts) * blockDim.x)
+            __stcs(reinterpret_cast<uint4*>(dst) + c, __ldg(reinterpret_cast<const uint4*>(src) + c));
+        return;
+    }
+    const uint32_t y0 = crop & 0x7FFFu, x0 = (crop >> 15) & 0xFFFFu;
+    const uint32_t a0 = (3 * x0) & ~15u;
+    const uint32_t nch = ((3 * x0 + 3 * kWinRows + 15u) & ~15u) / 16 - a0 / 16;
+    const uint8_t* s0 = src + static_cast<uint64_t>(y0) * row_bytes + a0;
+    for (uint32_t t = part * blockDim.x + threadIdx.x; t < kWinRows * nch;
+         t += parts * blockDim.x) {
+        const uint32_t r = t / nch, c = t - r * nch;
+        __stcs(reinterpret_cast<uint4*>(dst + r * kWinRow) + c,
+               __ldg(reinterpret_cast<const uint4*>(s0 + static_cast<uint64_t>(r) * row_bytes) + c));
+    }
+}
+
 struct PackArgs {
     const uint32_t* final_step;  // final ids of the step, all learners
     uint32_t n_sends;
@@ -24,8 +49,11 @@ struct PackArgs {
     const uint8_t* shard;
     uint64_t shard_first;
     uint64_t sample_bytes;
-    uint64_t chunks;             // per sample
+    uint64_t chunks;
     uint8_t* out;
+    const uint32_t* aug;
+    uint32_t row_bytes;
+    uint64_t slot_bytes;
 };
 
 __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
@@ -34,15 +62,12 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
     uint64_t rem = t;
     uint32_t m = 0;
     while (m + 1 < a.n_sends && rem >= a.count[m]) rem -= a.count[m++];
-    const uint32_t id = a.final_step[a.list_first[m] + rem];
+    const uint32_t fi = a.list_first[m] + static_cast<uint32_t>(rem);
+    const uint32_t id = a.final_step[fi];
     const uint8_t* src = a.shard + (id - a.shard_first) * a.sample_bytes;
-    uint8_t* dst = a.out + t * a.sample_bytes;
-    const uint64_t b0 = c * kChunk;
-    const uint64_t b1 = b0 + kChunk < a.sample_bytes ? b0 + kChunk : a.sample_bytes;
-    for (uint64_t b = b0 + 16ull * threadIdx.x; b + 16 <= b1; b += 16ull * blockDim.x) {
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + b));
-        __stcs(reinterpret_cast<uint4*>(dst + b), v);
-    }
+    copy_slot(src, a.out + t * a.slot_bytes, a.sample_bytes, a.aug != nullptr,
+              a.aug ? a.aug[fi] : 0u, a.row_bytes, static_cast<uint32_t>(c),
+              static_cast<uint32_t>(a.chunks));
 }
 
 // Regular scheme (reg_slice, sampling.cpp:27-42) over NCCL: learner j's slice
@@ -63,8 +88,11 @@ struct RegPrepArgs {
     uint32_t p, me, L;
     const uint8_t* shard;
     uint64_t shard_first, sample_bytes;
-    uint8_t* pack;            // [p][L] samples
-    uint32_t* ridx;           // [L]: my slice position -> receive index or kLocal
+    uint8_t* pack;
+    uint32_t* ridx;
+    const uint32_t* aug;
+    uint32_t row_bytes;
+    uint64_t slot_bytes;
 };
 
 __global__ void __launch_bounds__(256) k_reg_prep(RegPrepArgs a) {
@@ -87,11 +115,9 @@ __global__ void __launch_bounds__(256) k_reg_prep(RegPrepArgs a) {
     }
     // o == me, j != me: copy the sample into message (j), slot rank
     const uint32_t id = a.batch[e];
-    const uint4* src = reinterpret_cast<const uint4*>(a.shard + (id - a.shard_first) * a.sample_bytes);
-    uint4* dst = reinterpret_cast<uint4*>(a.pack + (static_cast<uint64_t>(j) * a.L + rank) *
-                                                       a.sample_bytes);
-    const uint64_t n16 = a.sample_bytes / 16;
-    for (uint64_t c = threadIdx.x; c < n16; c += blockDim.x) __stcs(dst + c, __ldg(src + c));
+    copy_slot(a.shard + (id - a.shard_first) * a.sample_bytes,
+              a.pack + (static_cast<uint64_t>(j) * a.L + rank) * a.slot_bytes, a.sample_bytes,
+              a.aug != nullptr, a.aug ? a.aug[e] : 0u, a.row_bytes, 0, 1);
 }
 
 } // namespace
@@ -99,11 +125,12 @@ __global__ void __launch_bounds__(256) k_reg_prep(RegPrepArgs a) {
 void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scratch,
                      const uint32_t* d_regcnt, uint32_t p, uint32_t me, uint64_t B,
                      const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
-                     uint8_t* pack, uint32_t* ridx) {
+                     uint8_t* pack, uint32_t* ridx, const uint32_t* d_aug, uint32_t row_bytes) {
     require(sample_bytes % 16 == 0, "exchange: sample bytes must be a multiple of 16");
     require(B % p == 0, "reg_slice: learner count must divide the batch size");
     RegPrepArgs a{d_batch, d_scratch, d_regcnt, p, me, static_cast<uint32_t>(B / p), shard,
-                  shard_first, sample_bytes, pack, ridx};
+                  shard_first, sample_bytes, pack, ridx, d_aug, row_bytes,
+                  d_aug ? kWinBytes : sample_bytes};
     launch(ctx, "reg_prep", [&] {
         k_reg_prep<<<static_cast<unsigned>(B), 256, 0, ctx->stream>>>(a);
     });
@@ -111,7 +138,7 @@ void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scr
 
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
-                 uint8_t* packbuf) {
+                 uint8_t* packbuf, const uint32_t* d_aug, uint32_t row_bytes) {
     PackArgs a{};
     uint64_t n_pack = 0;
     for (const ll_xfer& x : xfers) {
@@ -127,8 +154,11 @@ void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t*
     a.shard = shard;
     a.shard_first = shard_first;
     a.sample_bytes = sample_bytes;
-    a.chunks = (sample_bytes + kChunk - 1) / kChunk;
+    a.slot_bytes = d_aug ? kWinBytes : sample_bytes;
+    a.chunks = (a.slot_bytes + kChunk - 1) / kChunk;
     a.out = packbuf;
+    a.aug = d_aug;
+    a.row_bytes = row_bytes;
     launch(ctx, "pack", [&] {
         k_pack<<<static_cast<unsigned>(n_pack * a.chunks), 256, 0, ctx->stream>>>(a);
     });

@@ -214,7 +214,16 @@ struct SrcMap {
     const uint8_t* storage = nullptr;
     // regular scheme over NCCL: list position -> recv index (0xFFFFFFFF: own shard)
     const uint32_t* recv_idx = nullptr;
+    // NCCL receive slots hold crop windows (kWinRows rows at recv_row pitch,
+    // from the 16-byte-aligned window start) when recv_row != 0, else samples
+    uint32_t recv_row = 0;
 };
+// NCCL messages carry a crop-mode sample as its crop window only: 224 rows of
+// the 16-byte-aligned span holding its 672 window bytes (<= 704 bytes), not
+// the whole 196,608-byte sample
+constexpr uint32_t kWinRows = 224;
+constexpr uint32_t kWinRow = 704;
+constexpr uint64_t kWinBytes = static_cast<uint64_t>(kWinRows) * kWinRow;
 // prepared_slot >= 0: the resize prologue already ran into buffer set
 // (owner, prepared_slot)
 void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uint64_t epoch,
@@ -239,13 +248,16 @@ std::vector<ll_xfer> exchange_plan(const ll_move* moves, uint32_t n, const uint6
 // regular scheme over NCCL: pack this learner's samples of other slices into
 // [p][B/p] messages, and map its own slice positions to receive indices
 // (0xFFFFFFFF = own shard)
+// d_aug (or null): the plan's packed crop parameters of the step, aligned with
+// d_batch / d_final_step; with it each message slot carries only the sample's
+// crop window (kWinBytes; image rows of row_bytes), else the whole sample
 void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scratch,
                      const uint32_t* d_regcnt, uint32_t p, uint32_t me, uint64_t B,
                      const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
-                     uint8_t* pack, uint32_t* ridx);
+                     uint8_t* pack, uint32_t* ridx, const uint32_t* d_aug, uint32_t row_bytes);
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
-                 uint8_t* packbuf);
+                 uint8_t* packbuf, const uint32_t* d_aug, uint32_t row_bytes);
 
 // train.cu: consumer side (equivalence.cpp:95-205) on the device
 void train_run_device(ll_ctx* ctx, const double* h_xs, const double* h_ys, uint64_t n,

@@ -233,17 +233,22 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
     require(c.geometry == LL_GEOM_FIXED, "loader: variable-size samples need the P2P exchange");
     const uint32_t* d_final_step = pd.final_ids + step * B;
     cudaStream_t main = ctx->stream;
+    // crop mode: messages carry crop windows (K6 reads nothing else of a sample)
+    const bool win = c.augment.mode == LL_AUG_CROP;
+    const uint64_t slot = win ? kWinBytes : ld->S;
+    const uint32_t* d_aug = win ? pd.aug + step * B : nullptr;
+    const uint32_t row_bytes = 3 * c.width;
     if (c.scheme == LL_SCHEME_REGULAR) {
         require(h_regcnt != nullptr && pd.regcnt != nullptr, "loader: regular plan lacks counts");
         const uint64_t L = B / p;
-        x.pack.reserve(B * ld->S);
-        x.recv.reserve(B * ld->S);
+        x.pack.reserve(B * slot);
+        x.recv.reserve(B * slot);
         x.ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(L, 1));
         ctx->stream = stream;
         try {
             reg_prep_device(ctx, d_final_step, pd.scratch + step * B, pd.regcnt + step * p * p, p,
                             me, B, ld->shard.as<uint8_t>(), ld->first, ld->S,
-                            x.pack.as<uint8_t>(), x.ridx.as<uint32_t>());
+                            x.pack.as<uint8_t>(), x.ridx.as<uint32_t>(), d_aug, row_bytes);
         } catch (...) {
             ctx->stream = main;
             throw;
@@ -254,10 +259,10 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
             if (r == me) continue;
             const uint64_t ns = h_regcnt[r * p + me], nr = h_regcnt[me * p + r];
             if (ns)
-                LL_NCCL(ncclSend(x.pack.as<uint8_t>() + r * L * ld->S, ns * ld->S, ncclUint8,
+                LL_NCCL(ncclSend(x.pack.as<uint8_t>() + r * L * slot, ns * slot, ncclUint8,
                                  static_cast<int>(r), ld->comm, stream));
             if (nr)
-                LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + r * L * ld->S, nr * ld->S, ncclUint8,
+                LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + r * L * slot, nr * slot, ncclUint8,
                                  static_cast<int>(r), ld->comm, stream));
         }
         LL_NCCL(ncclGroupEnd());
@@ -266,12 +271,12 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
     const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
     uint64_t n_send = 0, n_recv = 0;
     for (const ll_xfer& xf : xs) (xf.is_send ? n_send : n_recv) += xf.count;
-    x.pack.reserve(std::max<uint64_t>(n_send, 1) * ld->S);
-    x.recv.reserve(std::max<uint64_t>(n_recv, 1) * ld->S);
+    x.pack.reserve(std::max<uint64_t>(n_send, 1) * slot);
+    x.recv.reserve(std::max<uint64_t>(n_recv, 1) * slot);
     ctx->stream = stream;  // pack_device launches on the context stream
     try {
         pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
-                    x.pack.as<uint8_t>());
+                    x.pack.as<uint8_t>(), d_aug, row_bytes);
     } catch (...) {
         ctx->stream = main;
         throw;
@@ -280,10 +285,10 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
     LL_NCCL(ncclGroupStart());
     for (const ll_xfer& xf : xs) {
         if (xf.is_send)
-            LL_NCCL(ncclSend(x.pack.as<uint8_t>() + xf.buf_first * ld->S, xf.count * ld->S,
+            LL_NCCL(ncclSend(x.pack.as<uint8_t>() + xf.buf_first * slot, xf.count * slot,
                              ncclUint8, static_cast<int>(xf.peer), ld->comm, stream));
         else
-            LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + xf.buf_first * ld->S, xf.count * ld->S,
+            LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + xf.buf_first * slot, xf.count * slot,
                              ncclUint8, static_cast<int>(xf.peer), ld->comm, stream));
     }
     LL_NCCL(ncclGroupEnd());
@@ -379,6 +384,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
             x = &ld->xcur;
         }
         src.recv = x->recv.as<uint8_t>();
+        if (c.augment.mode == LL_AUG_CROP) src.recv_row = kWinRow;  // window slots
         if (reg) {
             src.recv_idx = x->ridx.as<uint32_t>();
             n_recv = nvl_recv = n_local - h_regcnt[me * p + me];
