@@ -122,6 +122,7 @@ struct ll_loader {
         bool synchronous = false;
         std::string rtag;                // owner name of this slot's K7 prologue set
         int rslot = -1;                  // K7 prologue prepared into (rtag, 0), or -1
+        std::vector<uint32_t> rc;        // regular + NCCL: the step's [slice][owner] counts
         Tables* tab() const { return reinterpret_cast<Tables*>(pin); }
         uint64_t* ids() const { return pin + sizeof(Tables) / 8; }
     };
@@ -1161,6 +1162,22 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             });
             LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab + sizeof(uint64_t) * h.n_local,
                                     cudaMemcpyDeviceToHost, ctx->stream));
+        } else {
+            // NCCL exchange / unbalanced lists: the host needs the counts to
+            // size the grid and the messages; staged here on the side stream so
+            // the host waits for this step's plan only, not for the previous
+            // step's augment on the main stream
+            launch(ctx, "stage", [&] {
+                k_stage<<<1, 256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), 0);
+            });
+            LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab, cudaMemcpyDeviceToHost, ctx->stream));
+            if (pd.regcnt) {
+                h.rc.resize(static_cast<size_t>(p) * p);
+                LL_CUDA(cudaMemcpyAsync(h.rc.data(), pd.regcnt, sizeof(uint32_t) * h.rc.size(),
+                                        cudaMemcpyDeviceToHost, ctx->stream));
+            } else {
+                h.rc.clear();
+            }
         }
         LL_CUDA(cudaEventRecord(h.pro_done, ctx->stream));
     } catch (...) {
@@ -1178,19 +1195,9 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
         h.info.d2h_bytes = tab + sizeof(uint64_t) * h.n_local;
         h.info.device_out = reinterpret_cast<uintptr_t>(out);
     } else {
-        // NCCL exchange / unbalanced lists: the host needs the counts to size
-        // the grid and the messages before issuing the rest of the step
-        launch(ctx, "stage", [&] {
-            k_stage<<<1, 256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), 0);
-        });
-        LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab, cudaMemcpyDeviceToHost, ctx->stream));
-        std::vector<uint32_t> rc;  // regular + NCCL: this step's [slice][owner] counts
-        if (pd.regcnt) {
-            rc.resize(static_cast<size_t>(p) * p);
-            LL_CUDA(cudaMemcpyAsync(rc.data(), pd.regcnt, sizeof(uint32_t) * rc.size(),
-                                    cudaMemcpyDeviceToHost, ctx->stream));
-        }
-        LL_CUDA(cudaStreamSynchronize(ctx->stream));
+        // the tables staged on the side stream (prologue above)
+        LL_CUDA(cudaEventSynchronize(h.pro_done));
+        const std::vector<uint32_t>& rc = h.rc;  // regular + NCCL: [slice][owner] counts
         const auto* t = h.tab();
         ll_step_info local{};
         run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local, nullptr,

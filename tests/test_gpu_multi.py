@@ -18,7 +18,8 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanced"):
+def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanced",
+            host=False):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
@@ -46,12 +47,27 @@ def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanc
     order = oracle.permute_epoch(seed, 1, d)
     bad = []
     received = 0
-    for t in [0, 1, 17, ld.steps_per_epoch - 1]:
-        info = ld.step(1, t)
+    steps = [0, 1, 17, ld.steps_per_epoch - 1]
+    if host:
+        # host-driven path (ll_loader_submit_host / wait_host), two steps in
+        # flight: the next step's plan is staged while the previous one runs
+        host_ids = np.empty(B, np.uint64)
+        ld.submit_host(1, steps[0], order[steps[0] * B:(steps[0] + 1) * B])
+    for i, t in enumerate(steps):
+        if host:
+            if i + 1 < len(steps):
+                n = steps[i + 1]
+                ld.submit_host(1, n, order[n * B:(n + 1) * B])
+            info = ld.wait_host(host_ids)
+        else:
+            info = ld.step(1, t)
         mode = (oracle.MODE_REGULAR if scheme == "regular" else oracle.MODE_LOCALITY_BALANCED)
         r = oracle.assign_step(order[t * B:(t + 1) * B], world, d, mode)
         lst = r["final_ids"][r["final_off"][rank]:r["final_off"][rank + 1]]
         got_ids = ld.fetch_ids(info)
+        if host and not np.array_equal(host_ids[:info.n_local], lst):
+            bad.append(f"step {t}: host ids differ")
+            continue
         if not np.array_equal(got_ids, lst):
             bad.append(f"step {t}: ids differ")
             continue
@@ -109,6 +125,25 @@ def test_four_learners_exchange(tmp_path, exchange, scheme):
     import torch.multiprocessing as mp
     world = 4
     mp.spawn(_worker, args=(world, _free_port(), exchange, "bf16", str(tmp_path), scheme),
+             nprocs=world, join=True)
+    total_recv = 0
+    for r in range(world):
+        lines = open(tmp_path / f"rank{r}.txt").read().splitlines()
+        total_recv += int(lines[0].split()[1])
+        assert lines[1:] == [], lines[1:]
+    assert total_recv > 0
+
+
+@pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("exchange,scheme", [("nccl", "locality_balanced"),
+                                             ("nccl", "regular"),
+                                             ("p2p", "locality_balanced")])
+def test_two_learners_host_path(tmp_path, exchange, scheme):
+    """The reference-facing host call (GlobalBatch from host memory, two steps
+    in flight) with the exchange: same outputs as the device-driven steps."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), exchange, "bf16", str(tmp_path), scheme, True),
              nprocs=world, join=True)
     total_recv = 0
     for r in range(world):
