@@ -1200,8 +1200,29 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
         const std::vector<uint32_t>& rc = h.rc;  // regular + NCCL: [slice][owner] counts
         const auto* t = h.tab();
         ll_step_info local{};
-        run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local, nullptr,
+        // NCCL: the exchange goes on the side stream behind this step's
+        // prologue, into one of two buffer sets, so it overlaps the previous
+        // step's augment on the main stream
+        const ll_loader::ExSet* pre = nullptr;
+        int xs = -1;
+        if (p > 1 && c.exchange == LL_EXCHANGE_NCCL) {
+            if (!ld->xdone[0]) {
+                for (int i = 0; i < 2; ++i) {
+                    LL_CUDA(cudaEventCreateWithFlags(&ld->xdone[i], cudaEventDisableTiming));
+                    LL_CUDA(cudaEventCreateWithFlags(&ld->augdone[i], cudaEventDisableTiming));
+                }
+            }
+            xs = static_cast<int>(ld->submitted & 1);
+            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[xs], 0));
+            issue_exchange(ld, pd, 0, t->moves, t->n, t->off, rc.empty() ? nullptr : rc.data(),
+                           ld->xset[xs], ld->side);
+            LL_CUDA(cudaEventRecord(ld->xdone[xs], ld->side));
+            LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[xs], 0));
+            pre = &ld->xset[xs];
+        }
+        run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local, pre,
                  -1, rc.empty() ? nullptr : rc.data());
+        if (xs >= 0) LL_CUDA(cudaEventRecord(ld->augdone[xs], ctx->stream));
         local.h2d_bytes = h.info.h2d_bytes;
         local.d2h_bytes = tab + sizeof(uint32_t) * rc.size();
         h.info = local;
