@@ -129,8 +129,7 @@ def workload(args, n):
             "per_gpu_batch": args.per_gpu_batch, "alpha": alpha_for(args, n),
             "scheme": "regular" if args.workload == "cfg4" else "locality_balanced",
             "exchange": args.exchange if n > 1 else "none", "out_dtype": args.dtype,
-            "l2": "inputs larger than L2 (31.5 GB shard, 616 MB output/step); no flush",
-            "timed_region": "starts at an epoch boundary; epoch plans included"}
+            "l2": "inputs larger than L2 (31.5 GB shard, 616 MB output/step); no flush"}
 
 
 # ------------------------------------------------------------------ clocks
@@ -249,23 +248,79 @@ def cpu_reference_run(args, n, steps, warmup, seconds_cap=None):
 
 
 def remote_summary(args, n, d, B, totals):
-    """Remote samples per epoch: locality-balanced moves (measured from the
-    device plan) vs the regular scheme's remote samples (counted in the same
-    plan) vs the paper's model, Eq. 7 (alpha*D*(p-1)/p) and Eq. 8
-    (alpha*D*beta) with beta measured as moved/B (model.hpp:65-74)."""
+    """Remote samples per epoch of THIS run's workload (p = N learners):
+    locality-balanced moves and the regular scheme's remote samples, both
+    counted by K4 in the run's own device plan."""
     per = mean_window_bytes_cfg5() if args.workload == "cfg5" else H * W * 3
     steps = d // B
-    beta = totals["moved"] / (steps * B) if steps else 0.0
-    return {"loc_moved_samples": totals["moved"],
+    D = steps * B
+    return {"p": n, "d": d, "B": B, "samples_per_epoch": D,
+            "loc_moved_samples": totals["moved"],
             "loc_nvlink_samples": totals["moved_nvlink"],
             "reg_remote_samples": totals["reg_remote"],
-            "eq7_samples": d * (n - 1) / n, "eq8_samples": d * beta, "beta": beta,
             "bytes_per_sample": per,
             "loc_remote_bytes": totals["moved_nvlink"] * per,
             "reg_remote_bytes": totals["reg_remote"] * per,
-            "local_fraction": 1.0 - (totals["moved"] / (steps * B) if steps else 0.0),
+            "eq7_samples": alpha_for(args, n) * D * (n - 1) / n,
+            "local_fraction": 1.0 - (totals["moved"] / D if D else 0.0),
             "storage_samples": totals["uncached"],
             "storage_window_bytes": totals["uncached"] * src_bytes_per_sample(args)}
+
+
+HEADLINE_D = 1_280_000
+
+
+def eq8_betas() -> dict:
+    """Eq. 8's predicted beta per p: the median of the reference's
+    simulate_imbalance (simulate.cpp:42-79) run the way `locload imbalance`
+    runs it (500 steps, seed derive_seed(42, p, 1024)), computed by running
+    oracle/_ref in the build container and committed as a fixture
+    (tests/golden/make_golden.py); the bench only reads the number."""
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        g = json.load(f)
+    return {c["p"]: c["beta_median"] for c in g["simulate_imbalance"]
+            if c["d"] == HEADLINE_D and c["local_batch"] == 1024}
+
+
+def headline_remote(device: int, seed: int = SEED, epoch: int = 0) -> dict:
+    """Remote bytes per epoch at the headline configuration (cfg2: d = 1.28 M,
+    B = 1,024 p) for p = 2 / 4 / 8, from the device plan (ll_plan_epoch: K2+K3
+    + K4 over the whole epoch -- the plan is replicated, so one GPU computes
+    every learner's share).  Loc = samples the balancer moves; Reg = samples
+    reg_slice hands to a non-owner (naive DistributedSampler, cfg4).  Model
+    (model.hpp:65-74): Eq. 7 alpha*D*(p-1)/p, Eq. 8 alpha*D*beta_median with
+    beta from the reference's simulate_imbalance (eq8_betas), D = steps * B
+    samples per epoch (remainder dropped, core.cpp:57-73)."""
+    import paper_1910_01196_b200 as ll
+    betas = eq8_betas()
+    whole, window, msg = H * W * 3, SRC_BYTES, 157_696  # NCCL crop-window slot
+    out = {"seed": seed, "epoch": epoch, "d": HEADLINE_D, "alpha": 1.0,
+           "bytes_per_sample": {"whole": whole, "crop_window": window,
+                                "nccl_window_slot": msg},
+           "model": "Eq. 7 = alpha*D*(p-1)/p, Eq. 8 = alpha*D*beta_median (model.hpp:65-74); "
+                    "beta_median from reference simulate_imbalance (500 steps, "
+                    "derive_seed(42, p, 1024))", "p": {}}
+    for p in (2, 4, 8):
+        B = 1024 * p
+        t0 = time.perf_counter()
+        plan = ll.plan_epoch(seed, epoch, HEADLINE_D, p, B, device=device, with_ids=False)
+        ms = (time.perf_counter() - t0) * 1e3
+        D = plan.steps * B
+        moved, reg = int(plan.totals[0]), int(plan.totals[3])
+        beta = betas.get(p)
+        eq8 = D * beta if beta is not None else None
+        out["p"][str(p)] = {
+            "B": B, "steps": plan.steps, "samples_per_epoch": D,
+            "loc_moved_samples": moved, "loc_moved_bytes_whole": moved * whole,
+            "loc_moved_bytes_window": moved * window,
+            "reg_remote_samples": reg, "reg_remote_bytes_whole": reg * whole,
+            "reg_remote_bytes_window": reg * window,
+            "eq7_samples": D * (p - 1) / p, "eq8_samples": eq8, "beta_median": beta,
+            "beta_measured": moved / D, "loc_vs_eq8": moved / eq8 if eq8 else None,
+            "reg_vs_eq7": reg / (D * (p - 1) / p),
+            "loc_over_reg_bytes": moved / reg if reg else None,
+            "local_fraction": 1.0 - moved / D, "plan_wall_ms": ms}
+    return out
 
 
 def run_reference(args):
@@ -368,6 +423,13 @@ def run_ours(args):
     barrier()
 
     # ---- timed region (value) ----
+    # The dominant kernel's launches are bracketed by CUDA events on the
+    # stream they run on (the library's launch hook), inside this same region,
+    # so roofline.achieved and value describe the same launches.
+    # LL_BENCH_NO_KERNEL_EVENTS=1 times the region without them (A/B).
+    kernel_events = not os.environ.get("LL_BENCH_NO_KERNEL_EVENTS")
+    _capi.check(lib.ll_ctx_reset_stats(ctx))
+    _capi.check(lib.ll_ctx_set_timing(ctx, 1 if kernel_events else 0))
     launches0 = C.c_uint64()
     _capi.check(lib.ll_ctx_launch_count(ctx, C.byref(launches0)))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -382,26 +444,29 @@ def run_ours(args):
         barrier()
     launches1 = C.c_uint64()
     _capi.check(lib.ll_ctx_launch_count(ctx, C.byref(launches1)))
+    _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     total_samples = sum_over_ranks(samples)
     value = total_samples / (ms / 1e3)
-
-    # ---- dominant kernel: live CUDA-event timing of augment_crop ----
-    _capi.check(lib.ll_ctx_reset_stats(ctx))
-    _capi.check(lib.ll_ctx_set_timing(ctx, 1))
-    k2 = min(args.steps, 2 * spe)
-    start2 = start + ((args.steps + spe - 1) // spe) * spe  # fresh epochs: plans re-run
-    barrier()
-    run_steps(start2, k2)
-    barrier()
-    _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     stats = {}
-    for name in [aug_kernel, "permute", "assign", "pack", "resize_prep", "resize_pull"]:
+    for name in [aug_kernel, "permute", "assign", "pack", "reg_prep", "resize_prep",
+                 "resize_pull"]:
         cnt, tot = C.c_uint64(), C.c_double()
         _capi.check(lib.ll_ctx_kernel_stats(ctx, name.encode(), C.byref(cnt), C.byref(tot)))
         stats[name] = (cnt.value, tot.value)
     aug_n, aug_ms = stats[aug_kernel]
+    e_first, s_first = divmod(start, spe)
+    e_last, s_last = divmod(start + args.steps - 1, spe)
+    n_plans = stats["permute"][0]
+    timed_region = (f"{args.steps} steps from epoch {e_first} step {s_first} to epoch {e_last} "
+                    f"step {s_last} ({spe} steps per epoch); {n_plans} epoch plan(s) "
+                    "(K2+K3 permutation + K4 assignment of a whole epoch, prefetched at "
+                    "mid-epoch on the plan stream) computed inside"
+                    + ("" if n_plans else "; this region's own epoch plan was prefetched "
+                       "before it (during warm-up / population)"))
     per_launch_bytes = args.per_gpu_batch * (src_bytes_per_sample(args) + out_bytes(args.dtype))
+    if not kernel_events:  # no per-launch events: the whole step as the launch time
+        aug_n, aug_ms = args.steps, ms
     achieved = per_launch_bytes / (aug_ms / aug_n / 1e3) / 1e9 if aug_n else 0.0
     achieved = max_over_ranks(-achieved) * -1 if dist is not None else achieved  # min over ranks
     peak = 6544.3
@@ -500,11 +565,15 @@ def run_ours(args):
                    "peak_source": "measured here: pinned host -> device copy-engine "
                                   "bandwidth (torch copy_ of 512 MiB, best of 5, CUDA events)",
                    "note": "zero-copy reads of the crop windows by the augment kernel"}
+    headline = None
+    if rank == 0 and not os.environ.get("LL_BENCH_NO_HEADLINE_PLAN"):
+        headline = headline_remote(local)
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                "dtype": args.dtype, "data": "synthetic", "config": workload(args, n),
+                "dtype": args.dtype, "data": "synthetic",
+                "config": dict(workload(args, n), timed_region=timed_region),
                 "clocks": clk.summary(),
                 "e2e": e2e,
                 "gpu_launches": int(launches1.value - launches0.value),
@@ -514,11 +583,17 @@ def run_ours(args):
                              "traffic": traffic, "peak_source": peak_src,
                              "algorithmic_bytes_per_launch": per_launch_bytes,
                              "avg_launch_ms": aug_ms / aug_n if aug_n else None,
-                             "launches_timed": aug_n},
+                             "launches_timed": aug_n,
+                             "timing": ("CUDA events around each launch on its stream, "
+                                        "inside the timed region of `value`"
+                                        if kernel_events else
+                                        "no per-launch events: ms_per_step as launch time"),
+                             "share_of_step": (aug_ms / ms) if kernel_events else 1.0},
                 "storage_roofline": storage,
                 "kernel_ms": {k: (v[1] / v[0] if v[0] else None) for k, v in stats.items()},
                 "cpu_baseline": cpu,
-                "remote_per_epoch": remote_summary(args, n, d, B, totals)}
+                "remote_per_epoch": dict(remote_summary(args, n, d, B, totals),
+                                         headline=headline)}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()

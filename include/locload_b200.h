@@ -111,6 +111,20 @@ int ll_assign(ll_ctx* ctx, const uint64_t* host_batch, uint64_t B, uint64_t d, u
               uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves,
               uint64_t* stats4);
 
+/* A whole epoch's plan on the device, no shard needed: permute_epoch
+ * (core.cpp:11-27) + batches (core.cpp:57-73, remainder dropped) + the
+ * ll_assign composition for every one of steps = d / B batches -- the
+ * sampler half of Loader::run_epoch (pipeline.cpp:251-252) composed with
+ * equivalence.cpp:66-91.  Outputs (host, each may be NULL):
+ * final_ids[steps*B], final_off[steps*(p+1)], kept[steps*p], counts[steps*p],
+ * moves[steps*p] (step s's n_moves[s] moves at s*p), stats4 = epoch totals
+ * {moved, moved over NVLink, uncached, regular-scheme remote (UINT64_MAX when
+ * p does not divide B)}. */
+int ll_plan_epoch(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint64_t d, uint32_t p,
+                  uint64_t B, double alpha, int scheme, uint64_t* steps_out,
+                  uint64_t* final_ids, uint64_t* final_off, uint64_t* kept, uint64_t* counts,
+                  ll_move* moves, uint32_t* n_moves, uint64_t* stats4);
+
 /* balance() on n independent instances (balance.cpp:58-84): counts/targets are
  * [n][p] row-major; moves [n][p]; n_moves[n].  Rejects mismatched sums with
  * balance.cpp:38-39's message. */

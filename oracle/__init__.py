@@ -159,6 +159,8 @@ def ref() -> C.CDLL:
                                               C.c_uint64, f64p]
         L.ref_sample_gradient.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, f64p, C.c_uint64,
                                           f64p, f64p]
+        L.ref_simulate_imbalance.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
+                                             C.c_uint64, C.c_double, f64p, f64p]
         _ref = L
     return _ref
 
@@ -346,6 +348,28 @@ def ref_assign_balanced(batch, d: int, p: int):
                                          _p(off, C.c_uint64), _p(moves, C.c_int64), C.byref(n)))
     mv = [tuple(int(x) for x in moves[3 * k:3 * k + 3]) for k in range(n.value)]
     return lists[:len(b)], off, mv
+
+
+def ref_simulate_imbalance(d: int, p: int, local_batch: int, steps: int, seed: int,
+                           alpha: float = 1.0):
+    """simulate_imbalance (simulate.cpp:42-79): per-step betas and the summary
+    {median, q1, q3, whisker_lo, whisker_hi}."""
+    betas = np.empty(max(steps, 1), np.float64)
+    summ = np.empty(5, np.float64)
+    f64p = C.POINTER(C.c_double)
+    _ref_check(ref().ref_simulate_imbalance(d, p, local_batch, steps, seed, alpha,
+                                            _p(betas, C.c_double), _p(summ, C.c_double)))
+    return betas[:steps], summ
+
+
+def eq8_beta_median(d: int, p: int, local_batch: int, seed: int = 42, steps: int = 500,
+                    alpha: float = 1.0) -> float:
+    """The predicted beta of Eq. 8 (model.hpp:72-74) the way the reference's
+    `locload imbalance` subcommand draws it: simulate_imbalance with `steps`
+    (default 500, locload.cpp:152) fresh batches and the per-cell seed
+    derive_seed(seed, p, local_batch) (locload.cpp:170); the summary median."""
+    s = int(ref().ref_derive_seed3(seed, p, local_batch))
+    return float(ref_simulate_imbalance(d, p, local_batch, steps, s, alpha)[1][0])
 
 
 def ref_loc_distribution(batch, d: int, p: int, alpha: float):

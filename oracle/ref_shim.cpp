@@ -23,6 +23,7 @@
 #include "locload/pipeline.hpp"
 #include "locload/rng.hpp"
 #include "locload/sampling.hpp"
+#include "locload/simulate.hpp"
 
 using namespace locload;
 
@@ -305,6 +306,23 @@ int ref_sample_gradient(uint64_t n, uint32_t dims, uint64_t obj_seed, const doub
         obj.sample_gradient(wv, i, g);
         std::memcpy(out, g.data(), sizeof(double) * dims);
         *loss = obj.sample_loss(wv, i);
+    });
+}
+
+// simulate_imbalance (simulate.cpp:42-79): the per-step balancing fractions
+// beta of `steps` fresh global batches and their five-number summary
+// {median, q1, q3, whisker_lo, whisker_hi} -- Eq. 8's predicted beta
+// (model.hpp:72-74).  betas may be NULL.
+int ref_simulate_imbalance(uint64_t d, uint32_t p, uint64_t local_batch, uint64_t steps,
+                           uint64_t seed, double alpha, double* betas, double* summary5) {
+    return guarded([&] {
+        const ImbalanceStats st = simulate_imbalance(d, p, local_batch, steps, seed, alpha);
+        if (betas) std::memcpy(betas, st.betas.data(), sizeof(double) * st.betas.size());
+        summary5[0] = st.summary.median;
+        summary5[1] = st.summary.q1;
+        summary5[2] = st.summary.q3;
+        summary5[3] = st.summary.whisker_lo;
+        summary5[4] = st.summary.whisker_hi;
     });
 }
 

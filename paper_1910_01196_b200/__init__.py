@@ -9,7 +9,8 @@ from . import _capi  # noqa: F401
 from .locload import (CacheDirectory, EpochPermutation, GlobalBatch, ImbalanceVector,  # noqa: F401
                       LocalAssignment, LocDistribution, Move, TransferSchedule, assign,
                       assign_batch, balance, balance_many, batches, counts_with_uncached,
-                      deficit_fraction, loc_distribution, permutation_prefix, permute_epoch,
+                      EpochPlan, deficit_fraction, loc_distribution, permutation_prefix,
+                      permute_epoch, plan_epoch,
                       reg_slice, targets)
 from .loader import AugmentConfig, DeviceLoader, LoaderConfig, ThroughputReport  # noqa: F401
 

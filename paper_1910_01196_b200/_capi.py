@@ -90,6 +90,9 @@ PROTOTYPES = {
     "ll_last_permute_profile": (C.c_int, [C.c_void_p, u64p]),
     "ll_assign": (C.c_int, [C.c_void_p, u64p, C.c_uint64, C.c_uint64, C.c_uint32, C.c_double,
                             C.c_int, u64p, u64p, u64p, u64p, C.POINTER(Move), u32p, u64p]),
+    "ll_plan_epoch": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
+                                C.c_uint64, C.c_double, C.c_int, u64p, u64p, u64p, u64p, u64p,
+                                C.POINTER(Move), u32p, u64p]),
     "ll_balance_batch": (C.c_int, [C.c_void_p, i64p, i64p, C.c_uint32, C.c_uint64,
                                    C.POINTER(Move), u32p]),
     "ll_exchange_plan": (C.c_int, [C.POINTER(Move), C.c_uint32, u64p, C.c_uint32, C.c_uint32,

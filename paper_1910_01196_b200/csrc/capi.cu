@@ -329,6 +329,77 @@ int ll_assign(ll_ctx* ctx, const uint64_t* host_batch, uint64_t B, uint64_t d, u
     });
 }
 
+// A whole epoch's plan with no shard attached: K2+K3 permute_epoch
+// (core.cpp:11-27), batches (core.cpp:57-73) and K4 over every step -- the
+// same kernels and device tables a loader plans its epochs with
+// (loader.cu plan_into), so tests can pin the headline configuration's plan
+// (cfg2: d = 1.28 M, p = 8, B = 8,192) and the bench can count remote samples
+// per epoch for any p on one GPU.
+int ll_plan_epoch(ll_ctx* ctx, uint64_t seed, uint64_t epoch, uint64_t d, uint32_t p,
+                  uint64_t B, double alpha, int scheme, uint64_t* steps_out,
+                  uint64_t* final_ids, uint64_t* final_off, uint64_t* kept, uint64_t* counts,
+                  ll_move* moves, uint32_t* n_moves, uint64_t* stats4) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(d != 0, "permute_epoch: dataset must contain at least one sample");
+        require(B != 0 && B <= d, "batches: batch size must be in [1, dataset size]");
+        require(p != 0, "CacheDirectory: learner count must be >= 1");
+        require(alpha > 0.0 && alpha <= 1.0, "CacheDirectory: cached fraction must be in (0, 1]");
+        require(p <= kMaxP, "assign: learner count must be in [1, 64]");
+        require(d < 0xFFFFFFFFull, "plan_epoch: dataset size must be < 2^32 - 1 on the device");
+        require(scheme >= LL_SCHEME_REGULAR && scheme <= LL_SCHEME_LOCALITY_BALANCED,
+                "assign: unknown scheme");
+        if (scheme == LL_SCHEME_REGULAR)
+            require(B % p == 0, "reg_slice: learner count must divide the batch size");
+        uint64_t cached = static_cast<uint64_t>(alpha * static_cast<double>(d));  // sampling.cpp:15
+        if (cached > d) cached = d;
+        const uint64_t steps = d / B;
+        if (steps_out) *steps_out = steps;
+        DevBuf& order = ctx->buf("epoch.order", sizeof(uint32_t) * d);
+        PlanBufs pb;
+        pb.reserve(steps, B);
+        permute_device(ctx, seed, epoch, static_cast<uint32_t>(d), order.as<uint32_t>(), nullptr,
+                       0, "epoch");
+        assign_device(ctx, order.as<uint32_t>(), steps, B, p, cached, scheme, pb.view());
+        std::vector<uint32_t> ids(final_ids ? steps * B : 0), off(steps * (kMaxP + 1)),
+            kp(steps * kMaxP), cn(steps * kMaxP), nm(steps), st(steps * 4);
+        std::vector<ll_move> mv(steps * kMaxP);
+        auto d2h = [&](void* dst, const DevBuf& b, size_t n) {
+            if (n) LL_CUDA(cudaMemcpyAsync(dst, b.ptr, n, cudaMemcpyDeviceToHost, ctx->stream));
+        };
+        d2h(ids.data(), pb.final_ids, sizeof(uint32_t) * ids.size());
+        d2h(off.data(), pb.off, sizeof(uint32_t) * off.size());
+        d2h(kp.data(), pb.kept, sizeof(uint32_t) * kp.size());
+        d2h(cn.data(), pb.counts, sizeof(uint32_t) * cn.size());
+        d2h(mv.data(), pb.moves, sizeof(ll_move) * mv.size());
+        d2h(nm.data(), pb.n_moves, sizeof(uint32_t) * nm.size());
+        d2h(st.data(), pb.stats, sizeof(uint32_t) * st.size());
+        LL_CUDA(cudaStreamSynchronize(ctx->stream));
+        permute_rounds(ctx, "epoch");  // raises if the round guard tripped
+        for (uint64_t i = 0; i < ids.size(); ++i) final_ids[i] = ids[i];
+        if (stats4)
+            for (int q = 0; q < 4; ++q) stats4[q] = 0;
+        for (uint64_t s = 0; s < steps; ++s) {
+            if (final_off)
+                for (uint32_t j = 0; j <= p; ++j)
+                    final_off[s * (p + 1) + j] = off[s * (kMaxP + 1) + j];
+            for (uint32_t j = 0; j < p; ++j) {
+                if (kept) kept[s * p + j] = kp[s * kMaxP + j];
+                if (counts) counts[s * p + j] = cn[s * kMaxP + j];
+            }
+            if (n_moves) n_moves[s] = nm[s];
+            if (moves)
+                for (uint32_t m = 0; m < nm[s]; ++m) moves[s * p + m] = mv[s * kMaxP + m];
+            if (stats4)
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t v = st[s * 4 + q];
+                    if (v == 0xFFFFFFFFu) stats4[q] = UINT64_MAX;
+                    else if (stats4[q] != UINT64_MAX) stats4[q] += v;
+                }
+        }
+    });
+}
+
 // balance.cpp:32-41 (validate) + :58-84
 int ll_balance_batch(ll_ctx* ctx, const int64_t* counts, const int64_t* targets, uint32_t p,
                      uint64_t n, ll_move* moves, uint32_t* n_moves) {

@@ -42,6 +42,14 @@ struct DevBuf {
         LL_CUDA(cudaMalloc(&ptr, n));
         bytes = n;
     }
+    // step-path check: buffers sized up front must never grow there (a
+    // cudaFree + cudaMalloc synchronises the device mid-step)
+    void need(size_t n, const char* what) const {
+        if (n > bytes)
+            fail(LL_ERR_RUNTIME, std::string("loader: ") + what + " needs " + std::to_string(n) +
+                                     " bytes but holds " + std::to_string(bytes) +
+                                     " (preallocated at setup; never grown on the step path)");
+    }
     template <typename T>
     T* as() const { return static_cast<T*>(ptr); }
     void release() {

@@ -84,7 +84,7 @@ struct ll_loader {
     // regular scheme, the slice-position -> receive-index map
     struct ExSet {
         ll::DevBuf pack, recv, ridx;
-    } xcur;
+    };
     // NCCL exchange of step t+1 issued on the side stream while step t's
     // augment runs (two buffer sets, alternating by step parity)
     ExSet xset[2];
@@ -122,7 +122,9 @@ struct ll_loader {
         bool synchronous = false;
         std::string rtag;                // owner name of this slot's K7 prologue set
         int rslot = -1;                  // K7 prologue prepared into (rtag, 0), or -1
-        std::vector<uint32_t> rc;        // regular + NCCL: the step's [slice][owner] counts
+        uint32_t* pin_rc = nullptr;      // regular + NCCL: the step's [slice][owner] counts
+                                         // (pinned: the D2H is queued behind the
+                                         // side stream's work, never a blocking copy)
         Tables* tab() const { return reinterpret_cast<Tables*>(pin); }
         uint64_t* ids() const { return pin + sizeof(Tables) / 8; }
     };
@@ -242,9 +244,9 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
     if (c.scheme == LL_SCHEME_REGULAR) {
         require(h_regcnt != nullptr && pd.regcnt != nullptr, "loader: regular plan lacks counts");
         const uint64_t L = B / p;
-        x.pack.reserve(B * slot);
-        x.recv.reserve(B * slot);
-        x.ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(L, 1));
+        x.pack.need(B * slot, "exchange send buffer");
+        x.recv.need(B * slot, "exchange receive buffer");
+        x.ridx.need(sizeof(uint32_t) * std::max<uint64_t>(L, 1), "exchange receive map");
         ctx->stream = stream;
         try {
             reg_prep_device(ctx, d_final_step, pd.scratch + step * B, pd.regcnt + step * p * p, p,
@@ -272,8 +274,8 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
     const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
     uint64_t n_send = 0, n_recv = 0;
     for (const ll_xfer& xf : xs) (xf.is_send ? n_send : n_recv) += xf.count;
-    x.pack.reserve(std::max<uint64_t>(n_send, 1) * slot);
-    x.recv.reserve(std::max<uint64_t>(n_recv, 1) * slot);
+    x.pack.need(n_send * slot, "exchange send buffer");
+    x.recv.need(n_recv * slot, "exchange receive buffer");
     ctx->stream = stream;  // pack_device launches on the context stream
     try {
         pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
@@ -379,11 +381,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     const bool reg = p > 1 && c.scheme == LL_SCHEME_REGULAR;
     if (p > 1 && c.exchange == LL_EXCHANGE_NCCL && (reg || ss.n_send || ss.n_recv)) {
         const ll_loader::ExSet* x = prefetched;
-        if (!x) {
-            issue_exchange(ld, pd, step, h_moves, h_nmoves, h_off, h_regcnt, ld->xcur,
-                           ctx->stream);
-            x = &ld->xcur;
-        }
+        require(x != nullptr, "loader: NCCL step without an issued exchange");
         src.recv = x->recv.as<uint8_t>();
         if (c.augment.mode == LL_AUG_CROP) src.recv_row = kWinRow;  // window slots
         if (reg) {
@@ -575,6 +573,7 @@ void loader_destroy(ll_loader* ld) {
         auto& h = *hp;
         if (h.pin) cudaFreeHost(h.pin);
         if (h.pin_batch) cudaFreeHost(h.pin_batch);
+        if (h.pin_rc) cudaFreeHost(h.pin_rc);
         if (h.pro_done) cudaEventDestroy(h.pro_done);
         if (h.done) cudaEventDestroy(h.done);
     }
@@ -613,9 +612,12 @@ void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     const ll_loader_config& c = ld->cfg;
     const uint64_t B = c.batch_size, p = c.learners;
     const uint64_t share = (B + p - 1) / p;
-    for (ll_loader::ExSet* x : {&ld->xcur, &ld->xset[0], &ld->xset[1]}) {
-        x->pack.reserve(std::max<uint64_t>(B * ld->S, 16));
-        x->recv.reserve(std::max<uint64_t>((c.scheme == LL_SCHEME_REGULAR ? B : share) * ld->S, 16));
+    // the message slot issue_exchange uses: a crop window (which may exceed a
+    // small source's whole sample, e.g. 224 x 224) or the whole sample
+    const uint64_t slot = c.augment.mode == LL_AUG_CROP ? kWinBytes : ld->S;
+    for (ll_loader::ExSet* x : {&ld->xset[0], &ld->xset[1]}) {
+        x->pack.reserve(std::max<uint64_t>(B * slot, 16));
+        x->recv.reserve(std::max<uint64_t>((c.scheme == LL_SCHEME_REGULAR ? B : share) * slot, 16));
         x->ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(share, 1));
     }
     LL_CUDA(cudaDeviceSynchronize());
@@ -1115,7 +1117,11 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             h.order.reserve(sizeof(uint32_t) * B);
             h.stage.reserve(sizeof(ll_loader::Tables) + sizeof(uint64_t) * B);
             h.plan.reserve(1, B);
-            if (reg_nccl(c)) h.plan.reserve_regcnt(1, p);
+            if (reg_nccl(c)) {
+                h.plan.reserve_regcnt(1, p);
+                LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h.pin_rc),
+                                      sizeof(uint32_t) * p * p, 0));
+            }
         }
         ensure_side_stream(ld);
     }
@@ -1124,7 +1130,16 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     h.rslot = -1;
     h.info.epoch = epoch;
     h.info.step = step;
-    std::memcpy(h.pin_batch, host_batch, sizeof(uint64_t) * B);
+    // the caller's GlobalBatch: ids index the shard and the storage tier, so
+    // an id outside [0, d) would read past them -- refuse it here
+    for (uint64_t i = 0; i < B; ++i) {
+        const uint64_t id = host_batch[i];
+        if (id >= c.d)
+            fail(LL_ERR_INVALID, "Loader: batch sample id " + std::to_string(id) +
+                                     " out of range (dataset has " + std::to_string(c.d) +
+                                     " samples)");
+        h.pin_batch[i] = id;
+    }
     // prologue (H2D + assignment) on the side stream, so it overlaps the
     // previous step's augment; it may reuse this slot only after the step that
     // last used it has finished on the main stream
@@ -1171,13 +1186,9 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
                 k_stage<<<1, 256, 0, ctx->stream>>>(pd, me, p, h.stage.as<uint8_t>(), 0);
             });
             LL_CUDA(cudaMemcpyAsync(h.pin, h.stage.ptr, tab, cudaMemcpyDeviceToHost, ctx->stream));
-            if (pd.regcnt) {
-                h.rc.resize(static_cast<size_t>(p) * p);
-                LL_CUDA(cudaMemcpyAsync(h.rc.data(), pd.regcnt, sizeof(uint32_t) * h.rc.size(),
+            if (pd.regcnt)
+                LL_CUDA(cudaMemcpyAsync(h.pin_rc, pd.regcnt, sizeof(uint32_t) * p * p,
                                         cudaMemcpyDeviceToHost, ctx->stream));
-            } else {
-                h.rc.clear();
-            }
         }
         LL_CUDA(cudaEventRecord(h.pro_done, ctx->stream));
     } catch (...) {
@@ -1197,7 +1208,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
     } else {
         // the tables staged on the side stream (prologue above)
         LL_CUDA(cudaEventSynchronize(h.pro_done));
-        const std::vector<uint32_t>& rc = h.rc;  // regular + NCCL: [slice][owner] counts
+        const uint32_t* rc = pd.regcnt ? h.pin_rc : nullptr;  // regular + NCCL
         const auto* t = h.tab();
         ll_step_info local{};
         // NCCL: the exchange goes on the side stream behind this step's
@@ -1214,17 +1225,18 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             }
             xs = static_cast<int>(ld->submitted & 1);
             LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[xs], 0));
-            issue_exchange(ld, pd, 0, t->moves, t->n, t->off, rc.empty() ? nullptr : rc.data(),
-                           ld->xset[xs], ld->side);
+            // a loader_step prefetch parked in this set is clobbered now
+            ld->xpending[xs].valid = false;
+            issue_exchange(ld, pd, 0, t->moves, t->n, t->off, rc, ld->xset[xs], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[xs], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[xs], 0));
             pre = &ld->xset[xs];
         }
         run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local, pre,
-                 -1, rc.empty() ? nullptr : rc.data());
+                 -1, rc);
         if (xs >= 0) LL_CUDA(cudaEventRecord(ld->augdone[xs], ctx->stream));
         local.h2d_bytes = h.info.h2d_bytes;
-        local.d2h_bytes = tab + sizeof(uint32_t) * rc.size();
+        local.d2h_bytes = tab + (rc ? sizeof(uint32_t) * p * p : 0);
         h.info = local;
         h.n_local = local.n_local;
         launch(ctx, "stage", [&] {

@@ -16,7 +16,7 @@ from typing import Callable, List, Optional
 import numpy as np
 
 from . import _capi
-from ._capi import check, ptr
+from ._capi import InvalidArgument, check, ptr
 from .locload import context
 
 IMAGENET_MEAN = (0.485, 0.456, 0.406)
@@ -169,21 +169,38 @@ class DeviceLoader:
         check(_capi.lib().ll_loader_step(self._h, epoch, step, C.byref(info)))
         return info
 
+    def _host_batch(self, batch) -> np.ndarray:
+        b = np.ascontiguousarray(batch, dtype=np.uint64)
+        if b.ndim != 1 or b.size != self.cfg.batch_size:
+            raise InvalidArgument(f"Loader: a global batch holds batch_size = "
+                                  f"{self.cfg.batch_size} ids (got {b.size})")
+        return b
+
+    def _out_ids(self, out_ids: np.ndarray) -> np.ndarray:
+        # the library writes up to batch_size u64 ids
+        if (not isinstance(out_ids, np.ndarray) or out_ids.dtype != np.uint64 or
+                not out_ids.flags.c_contiguous or out_ids.size < self.cfg.batch_size):
+            raise InvalidArgument("Loader: out_ids must be a contiguous uint64 array of at "
+                                  f"least batch_size = {self.cfg.batch_size} elements")
+        return out_ids
+
     def step_host(self, epoch: int, step: int, batch: np.ndarray, out_ids: np.ndarray):
+        b, o = self._host_batch(batch), self._out_ids(out_ids)
         info = _capi.StepInfo()
-        check(_capi.lib().ll_loader_step_host(self._h, epoch, step, ptr(batch, C.c_uint64),
-                                              ptr(out_ids, C.c_uint64), C.byref(info)))
+        check(_capi.lib().ll_loader_step_host(self._h, epoch, step, ptr(b, C.c_uint64),
+                                              ptr(o, C.c_uint64), C.byref(info)))
         return info
 
     def submit_host(self, epoch: int, step: int, batch: np.ndarray) -> None:
         """Queue one host-driven step (at most prefetch_depth outstanding)."""
-        b = np.ascontiguousarray(batch, dtype=np.uint64)
+        b = self._host_batch(batch)
         check(_capi.lib().ll_loader_submit_host(self._h, epoch, step, ptr(b, C.c_uint64)))
 
     def wait_host(self, out_ids: np.ndarray):
         """Deliver the oldest outstanding host step: (info) with out_ids filled."""
+        o = self._out_ids(out_ids)
         info = _capi.StepInfo()
-        check(_capi.lib().ll_loader_wait_host(self._h, ptr(out_ids, C.c_uint64), C.byref(info)))
+        check(_capi.lib().ll_loader_wait_host(self._h, ptr(o, C.c_uint64), C.byref(info)))
         return info
 
     def plan_step(self, step: int):

@@ -170,6 +170,52 @@ def assign_batch(batch_samples, d: int, p: int, alpha: float, scheme: int,
     return Assignment(ids[:B], off[:p + 1], kept[:p], counts[:p], mv, stats)
 
 
+@dataclass
+class EpochPlan:
+    """A whole epoch's device plan (ll_plan_epoch): permute_epoch + batches +
+    the per-step assignment of every global batch."""
+    steps: int
+    B: int
+    p: int
+    final_ids: np.ndarray  # [steps][B]
+    final_off: np.ndarray  # [steps][p+1]
+    kept: np.ndarray       # [steps][p]
+    counts: np.ndarray     # [steps][p]
+    moves: list            # per step: [(sender, receiver, count, src_off, dst_off, nvlink)]
+    totals: np.ndarray     # {moved, nvlink, uncached, reg_remote}
+
+    def lists(self, step: int) -> List[np.ndarray]:
+        o = self.final_off[step]
+        return [self.final_ids[step, o[j]:o[j + 1]] for j in range(self.p)]
+
+
+def plan_epoch(seed: int, epoch: int, d: int, p: int, B: int, alpha: float = 1.0,
+               scheme: str = "locality_balanced", device: int = 0,
+               with_ids: bool = True) -> EpochPlan:
+    """The sampler half of Loader::run_epoch (pipeline.cpp:251-252) composed
+    with equivalence.cpp:66-91 for every step: K2+K3 then K4, on the device."""
+    if B == 0 or B > d:
+        raise InvalidArgument("batches: batch size must be in [1, dataset size]")
+    steps = d // B
+    sc = SchemeKind[scheme] if isinstance(scheme, str) else int(scheme)
+    ids = np.empty((steps, B), np.uint64) if with_ids else None
+    off = np.empty((steps, p + 1), np.uint64)
+    kept = np.empty((steps, max(p, 1)), np.uint64)
+    counts = np.empty((steps, max(p, 1)), np.uint64)
+    moves = (_capi.Move * (steps * max(p, 1)))()
+    nm = np.zeros(steps, np.uint32)
+    tot = np.zeros(4, np.uint64)
+    n_steps = C.c_uint64()
+    check(_capi.lib().ll_plan_epoch(context(device), seed, epoch, d, p, B, alpha, sc,
+                                    C.byref(n_steps), ptr(ids, C.c_uint64) if with_ids else None,
+                                    ptr(off, C.c_uint64), ptr(kept, C.c_uint64),
+                                    ptr(counts, C.c_uint64), moves, ptr(nm, C.c_uint32),
+                                    ptr(tot, C.c_uint64)))
+    mv = [[(m.sender, m.receiver, m.count, m.src_off, m.dst_off, m.nvlink)
+           for m in moves[s * p:s * p + int(nm[s])]] for s in range(steps)]
+    return EpochPlan(steps, B, p, ids, off, kept[:, :p], counts[:, :p], mv, tot)
+
+
 def reg_slice(batch: GlobalBatch, p: int, j: int, device: int = 0) -> LocalAssignment:
     """sampling.cpp:27-42."""
     if p == 0 or j >= p:

@@ -56,6 +56,31 @@ def reg_remote(batch, d, p):
     return int((owners != pos_learner).sum())
 
 
+def plan_step_digest(lists, off, moves) -> str:
+    """sha256 over one step's plan: the final lists (u64, learner-major), the
+    offsets[p+1] (u64) and the moves as (sender, receiver, count) i64 triples.
+    The GPU tests digest ll_plan_epoch's tables the same way."""
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(lists, dtype=np.uint64).tobytes())
+    h.update(np.ascontiguousarray(off, dtype=np.uint64).tobytes())
+    h.update(np.asarray([x for m in moves for x in m[:3]], dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+def ref_epoch_plan(d, p, B, seed, epoch):
+    """The reference's plan of one epoch (alpha = 1), step by step."""
+    order = oracle.ref_permute_epoch(seed, epoch, d)
+    steps = []
+    moved = reg = 0
+    for t in range(d // B):
+        batch = order[t * B:(t + 1) * B]
+        lists, off, mv = oracle.ref_assign_balanced(batch, d, p)
+        steps.append((lists, off, mv))
+        moved += sum(m[2] for m in mv)
+        reg += reg_remote(batch, d, p)
+    return order, steps, moved, reg
+
+
 def main() -> None:
     R = oracle.ref()
     g: dict = {"source": "oracle/_ref (reference sources compiled in place)"}
@@ -156,6 +181,24 @@ def main() -> None:
         remote.append({"d": d, "p": p, "B": B, "seed": seed, "epoch": epoch, "loc_moved": moved,
                        "reg_remote": reg})
     g["remote_per_epoch"] = remote
+
+    # the headline configuration's plan (cfg2 shape: d = 1.28 M, B = 1,024 p),
+    # whole epochs, per-step digests -- SURVEY 8(d), BASELINE.md section 4
+    plans = []
+    for d, p, B, seed, epoch in [(1280000, 2, 2048, 42, 0), (1280000, 4, 4096, 42, 0),
+                                 (1280000, 8, 8192, 42, 0), (1280000, 8, 8192, 7, 2)]:
+        _, steps, moved, reg = ref_epoch_plan(d, p, B, seed, epoch)
+        plans.append({"d": d, "p": p, "B": B, "seed": seed, "epoch": epoch, "steps": len(steps),
+                      "loc_moved": moved, "reg_remote": reg,
+                      "n_moves": [len(mv) for _, _, mv in steps],
+                      "step_sha256": [plan_step_digest(*st) for st in steps]})
+    g["epoch_plans"] = plans
+
+    # Eq. 8's predicted beta: simulate_imbalance the way `locload imbalance`
+    # runs it (500 steps, seed derive_seed(seed, p, local_batch))
+    g["simulate_imbalance"] = [
+        {"d": 1280000, "p": p, "local_batch": 1024, "steps": 500, "seed": 42,
+         "beta_median": oracle.eq8_beta_median(1280000, p, 1024, 42)} for p in (2, 4, 8)]
 
     with open(OUT, "w") as f:
         json.dump(g, f, separators=(",", ":"))

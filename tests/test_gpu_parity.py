@@ -380,6 +380,86 @@ def test_loader_cfg1_plan_vs_oracle(golden):
             assert tot["reg_remote"] == ref["reg_remote"] == 7468
 
 
+def _plan_step_digest(lists, off, moves) -> str:
+    # tests/golden/make_golden.py:plan_step_digest
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(lists, dtype=np.uint64).tobytes())
+    h.update(np.ascontiguousarray(off, dtype=np.uint64).tobytes())
+    h.update(np.asarray([x for m in moves for x in m[:3]], dtype=np.int64).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("case", range(4), ids=["p2", "p4", "p8", "p8-seed7-epoch2"])
+def test_headline_plan_vs_reference(golden, case):
+    """cfg2's plan pinned on the device: the whole epoch at d = 1.28 M,
+    B = 1,024 p (K2+K3 permutation, K4 distribution + Algorithm 1 + tail moves
+    for all 625 / 312 / 156 steps) equals the reference step by step -- the
+    committed per-step digests of oracle/_ref's loc_distribution, balance and
+    equivalence.cpp:77-88 tail moves, and, where oracle/_ref is present, a
+    live list-by-list comparison.  Epoch totals equal BASELINE.md section 4:
+    11,102 / 13,652 / 15,059 moved, 640,140 / 958,300 / 1,119,042 Reg remote."""
+    c = golden["epoch_plans"][case]
+    d, p, B, seed, epoch = c["d"], c["p"], c["B"], c["seed"], c["epoch"]
+    plan = ll.plan_epoch(seed, epoch, d, p, B)
+    assert plan.steps == c["steps"] == d // B
+    got = [_plan_step_digest(plan.final_ids[t], plan.final_off[t], plan.moves[t])
+           for t in range(plan.steps)]
+    bad = [t for t in range(plan.steps) if got[t] != c["step_sha256"][t]]
+    assert not bad, f"steps differing from the reference: {bad[:10]}"
+    assert [len(m) for m in plan.moves] == c["n_moves"]
+    assert int(plan.totals[0]) == c["loc_moved"]
+    assert int(plan.totals[1]) == c["loc_moved"]  # alpha = 1: every move crosses NVLink
+    assert int(plan.totals[2]) == 0
+    assert int(plan.totals[3]) == c["reg_remote"]
+    want = {(2, 42): (11102, 640140), (4, 42): (13652, 958300), (8, 42): (15059, 1119042)}
+    if (p, seed) in want:
+        assert (c["loc_moved"], c["reg_remote"]) == want[(p, seed)]
+    # every learner keeps >= 90 % of its samples local (north_star target)
+    assert 1 - c["loc_moved"] / (plan.steps * B) >= 0.90
+    if oracle.ref_available():
+        order = oracle.ref_permute_epoch(seed, epoch, d)
+        for t in range(0, plan.steps, 7):
+            lists, off, mv = oracle.ref_assign_balanced(order[t * B:(t + 1) * B], d, p)
+            assert np.array_equal(plan.final_ids[t], lists), t
+            assert np.array_equal(plan.final_off[t], off), t
+            assert [m[:3] for m in plan.moves[t]] == mv, t
+            for j in range(p):  # kept = the learner's own samples left after its tail moves
+                sent = sum(m[2] for m in mv if m[0] == j)
+                assert plan.kept[t][j] == plan.counts[t][j] - sent
+
+
+def test_headline_plan_regular_scheme_vs_reference():
+    """cfg4's comparator at the headline shape: the regular scheme's lists are
+    reg_slice (sampling.cpp:27-42) of every batch of the epoch."""
+    d, p, B = 1280000, 8, 8192
+    plan = ll.plan_epoch(42, 0, d, p, B, scheme="regular")
+    order = oracle.ref_permute_epoch(42, 0, d) if oracle.ref_available() else \
+        oracle.permute_epoch(42, 0, d)
+    for t in [0, 1, 77, 155]:
+        for j in range(p):
+            want = order[t * B + j * (B // p):t * B + (j + 1) * (B // p)]
+            assert np.array_equal(plan.lists(t)[j], want)
+    assert int(plan.totals[0]) == 0
+
+
+def test_remote_per_epoch_reference_goldens(golden):
+    """golden remote_per_epoch: Loc moved / Reg remote of whole epochs, counted
+    by running the reference, equal the device plan's totals."""
+    for c in golden["remote_per_epoch"]:
+        plan = ll.plan_epoch(c["seed"], c["epoch"], c["d"], c["p"], c["B"], with_ids=False)
+        assert int(plan.totals[0]) == c["loc_moved"], c
+        assert int(plan.totals[3]) == c["reg_remote"], c
+
+
+def test_plan_epoch_errors():
+    with pytest.raises(_capi.InvalidArgument, match="batches: batch size must be in"):
+        ll.plan_epoch(1, 0, 10, 2, 11)
+    with pytest.raises(_capi.InvalidArgument, match="reg_slice: learner count must divide"):
+        ll.plan_epoch(1, 0, 100, 3, 10, scheme="regular")
+    with pytest.raises(_capi.InvalidArgument, match="cached fraction"):
+        ll.plan_epoch(1, 0, 100, 2, 10, alpha=0.0)
+
+
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_loader_cfg1_outputs_vs_oracle(dtype):
     """Four learners on one GPU (P2P exchange over shared HBM): each learner's
@@ -571,6 +651,33 @@ def test_loader_host_submit_wait_pipelined():
             ld.submit_host(4, t + 2, order[(t + 2) * B:(t + 3) * B])
     with pytest.raises(ValueError, match="no host step"):
         ld.wait_host(ids)
+
+
+def test_loader_host_batch_validation():
+    """A caller's GlobalBatch is range-checked before the device reads the
+    shard with it: ids >= d, a short batch or a too-small out_ids buffer are
+    refused (nothing is queued), and the loader stays usable afterwards."""
+    d, p, B = 4096, 2, 256
+    lds = make_learners(d, p, B)
+    ld = lds[0]
+    order = ll.permute_epoch(42, 0, d).order
+    bad = order[:B].copy()
+    bad[17] = d
+    with pytest.raises(_capi.InvalidArgument, match="out of range"):
+        ld.submit_host(0, 0, bad)
+    bad[17] = 2 ** 32 + 5  # would truncate to a valid u32 id on the device
+    with pytest.raises(_capi.InvalidArgument, match="out of range"):
+        ld.submit_host(0, 0, bad)
+    with pytest.raises(_capi.InvalidArgument, match="batch_size"):
+        ld.submit_host(0, 0, order[:B - 1])
+    with pytest.raises(_capi.InvalidArgument, match="out_ids"):
+        ld.step_host(0, 0, order[:B], np.empty(B - 1, np.uint64))
+    with pytest.raises(_capi.InvalidArgument, match="out_ids"):
+        ld.step_host(0, 0, order[:B], np.empty(B, np.int64))
+    ids = np.empty(B, np.uint64)
+    info = ld.step_host(0, 0, order[:B], ids)
+    r = oracle.assign_step(order[:B], p, d, oracle.MODE_LOCALITY_BALANCED)
+    assert np.array_equal(ids[:info.n_local], r["final_ids"][r["final_off"][0]:r["final_off"][1]])
 
 
 @pytest.mark.parametrize("p,alpha", [(1, 0.25), (2, 0.5), (3, 0.37)])
