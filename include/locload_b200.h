@@ -44,6 +44,7 @@ enum { LL_GEOM_FIXED = 0, LL_GEOM_VARIABLE = 1 };
 
 typedef struct ll_ctx ll_ctx;       /* one CUDA device + stream + workspace   */
 typedef struct ll_loader ll_loader; /* one learner's HBM shard + epoch plan   */
+typedef struct ll_store ll_store;   /* HBM sample store (SampleCache)         */
 
 int ll_version(void);
 const char* ll_last_error(void);
@@ -205,6 +206,30 @@ int ll_toy_synthesize(uint64_t n, uint32_t dims, uint64_t seed, double* host_xs,
 int ll_full_batch_gradient(ll_ctx* ctx, const double* host_xs, const double* host_ys, uint64_t n,
                            uint32_t dims, const double* host_w, const uint64_t* host_batch,
                            uint64_t batch_size, double* host_grad);
+
+/* ---- sample store: SampleCache, pipeline.hpp:68-94 ---------------------- */
+/* The populate-on-first-touch cache of the reference's Loader, held in HBM:
+ * at most capacity_samples samples of one fixed size, no replacement
+ * (SampleCache::insert ignores inserts at capacity, pipeline.hpp:78-83); slabs
+ * are allocated as it fills, and an exhausted device also ends inserts.
+ * Lookups may run concurrently with each other and with inserts (the
+ * reference's shared_mutex, pipeline.hpp:90); every call is thread-safe. */
+int ll_store_create(ll_store** out, int device, uint64_t capacity_samples);
+int ll_store_destroy(ll_store* st);
+int ll_store_size(ll_store* st, uint64_t* out);              /* SampleCache::size  */
+/* the stored sample size (fixed by the first insert; 0 while empty) */
+int ll_store_sample_bytes(ll_store* st, uint64_t* out);
+/* found[i] = 1 when ids[i] is held (SampleCache::find, pipeline.hpp:72-76) */
+int ll_store_lookup(ll_store* st, const uint64_t* ids, uint64_t n, uint8_t* found);
+/* SampleCache::insert for n samples of sample_bytes each at host_ptrs[i]
+ * (copied on ctx's stream; complete and visible to every thread on return);
+ * held ids and ids past capacity are skipped; inserted[i] (may be NULL). */
+int ll_store_insert(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
+                    uint64_t sample_bytes, const uint8_t* const* host_ptrs, uint8_t* inserted);
+/* host copies of n held samples, contiguous in host_dst[n * sample_bytes]
+ * (one device gather + one D2H); LL_ERR_INVALID if an id is not held */
+int ll_store_gather(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
+                    uint8_t* host_dst);
 
 /* ---- loader: pipeline.hpp:46-128 ---------------------------------------- */
 typedef struct ll_loader_config {

@@ -135,6 +135,15 @@ PROTOTYPES = {
     "ll_loader_plan_step": (C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, u64p, u64p,
                                       C.POINTER(Move), u32p]),
     "ll_loader_epoch_totals": (C.c_int, [C.c_void_p, u64p]),
+    "ll_store_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_uint64]),
+    "ll_store_destroy": (C.c_int, [C.c_void_p]),
+    "ll_store_size": (C.c_int, [C.c_void_p, u64p]),
+    "ll_store_sample_bytes": (C.c_int, [C.c_void_p, u64p]),
+    "ll_store_lookup": (C.c_int, [C.c_void_p, u64p, C.c_uint64, C.POINTER(C.c_uint8)]),
+    "ll_store_insert": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_uint64, C.c_uint64,
+                                  C.POINTER(C.c_void_p), C.POINTER(C.c_uint8)]),
+    "ll_store_gather": (C.c_int, [C.c_void_p, C.c_void_p, u64p, C.c_uint64,
+                                  C.POINTER(C.c_uint8)]),
 }
 
 _lib = None

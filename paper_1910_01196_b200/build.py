@@ -19,7 +19,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 PER_FILE = {}
 
 SOURCES = ["capi.cu", "permute.cu", "assign.cu", "shard.cu", "augment.cu", "exchange.cu",
-           "loader.cu", "train.cu", "host/locload_api.cpp"]
+           "loader.cu", "train.cu", "store.cu", "host/locload_api.cpp",
+           "host/pipeline_api.cpp"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2,-Wall,-ffp-contract=off", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include"), "-I" + CSRC]

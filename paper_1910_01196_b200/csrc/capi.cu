@@ -34,6 +34,15 @@ void loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* inf
 void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
                       uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);
 void loader_epoch_totals(ll_loader* ld, uint64_t* out4);
+// store.cu
+void store_create(ll_store** out, int device, uint64_t capacity_samples);
+void store_destroy(ll_store* st);
+void store_size(ll_store* st, uint64_t* out);
+void store_sample_bytes(ll_store* st, uint64_t* out);
+void store_lookup(ll_store* st, const uint64_t* ids, uint64_t n, uint8_t* found);
+void store_insert(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
+                  uint64_t sample_bytes, const uint8_t* const* host_ptrs, uint8_t* inserted);
+void store_gather(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n, uint8_t* host_dst);
 
 namespace {
 thread_local std::string g_last_error;
@@ -658,6 +667,37 @@ int ll_loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint6
 }
 int ll_loader_epoch_totals(ll_loader* ld, uint64_t* out4) {
     return guarded([&] { loader_epoch_totals(ld, out4); });
+}
+
+// ---- sample store: SampleCache (pipeline.hpp:68-94) in HBM (store.cu) ----
+int ll_store_create(ll_store** out, int device, uint64_t capacity_samples) {
+    return guarded([&] { store_create(out, device, capacity_samples); });
+}
+
+int ll_store_destroy(ll_store* st) {
+    return guarded([&] { store_destroy(st); });
+}
+
+int ll_store_size(ll_store* st, uint64_t* out) {
+    return guarded([&] { store_size(st, out); });
+}
+
+int ll_store_sample_bytes(ll_store* st, uint64_t* out) {
+    return guarded([&] { store_sample_bytes(st, out); });
+}
+
+int ll_store_lookup(ll_store* st, const uint64_t* ids, uint64_t n, uint8_t* found) {
+    return guarded([&] { store_lookup(st, ids, n, found); });
+}
+
+int ll_store_insert(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
+                    uint64_t sample_bytes, const uint8_t* const* host_ptrs, uint8_t* inserted) {
+    return guarded([&] { store_insert(st, ctx, ids, n, sample_bytes, host_ptrs, inserted); });
+}
+
+int ll_store_gather(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
+                    uint8_t* host_dst) {
+    return guarded([&] { store_gather(st, ctx, ids, n, host_dst); });
 }
 
 } // extern "C"

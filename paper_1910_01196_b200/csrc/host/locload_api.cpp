@@ -18,9 +18,10 @@
 #include "locload/rng.hpp"
 #include "locload/sampling.hpp"
 #include "locload_b200.h"
+#include "api_internal.h"
 
 namespace locload {
-namespace {
+namespace detail {
 
 void check(int status) {
     if (status == LL_OK) return;
@@ -29,12 +30,14 @@ void check(int status) {
     throw std::runtime_error(msg);
 }
 
+namespace {
 struct ThreadContexts {
     std::map<int, ll_ctx*> by_device;
     ~ThreadContexts() {
         for (auto& kv : by_device) ll_ctx_destroy(kv.second);
     }
 };
+} // namespace
 
 ll_ctx* ctx() {
     thread_local ThreadContexts tc;
@@ -44,6 +47,12 @@ ll_ctx* ctx() {
     if (!c) check(ll_ctx_create(&c, dev));
     return c;
 }
+
+} // namespace detail
+
+namespace {
+using detail::check;
+using detail::ctx;
 
 struct Assigned {
     std::vector<std::uint64_t> ids, off, kept, counts, stats;

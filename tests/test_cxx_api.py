@@ -10,7 +10,8 @@ import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 BIN = os.path.join(HERE, "cxx", "_bin")
-SUITES = ["test_core", "test_sampling", "test_balance", "test_equivalence", "test_gpu_api"]
+SUITES = ["test_core", "test_sampling", "test_balance", "test_equivalence", "test_pipeline",
+          "test_gpu_api"]
 
 
 @pytest.mark.gpu
