@@ -474,6 +474,9 @@ def run_ours(args):
     # step is what the ncu launch list must agree with
     _capi.check(lib.ll_ctx_reset_stats(ctx))
     _capi.check(lib.ll_ctx_set_timing(ctx, 1))
+    nccl = n > 1 and args.exchange == "nccl"
+    if nccl:
+        ld.exchange_stats(reset=True)
     k2 = min(args.steps, 2 * spe)
     start2 = start + ((args.steps + spe - 1) // spe) * spe
     barrier()
@@ -484,6 +487,22 @@ def run_ours(args):
     barrier()
     _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     diag_ms = d0.elapsed_time(d1)
+    exchange = None
+    if nccl:
+        # NVLink GB/s of the NCCL exchange: message bytes this rank received
+        # / time from the grouped send/recv's issue to its completion on the
+        # side stream (CUDA events), min over ranks; it runs concurrently with
+        # the previous step's augment
+        xs = ld.exchange_stats(reset=True)
+        gbs = xs["wire_gbs"] or 0.0
+        gbs = max_over_ranks(-gbs) * -1 if dist is not None else gbs
+        exchange = {"backend": "nccl grouped send/recv", "steps_timed": xs["timed_steps"],
+                    "recv_bytes_per_step": xs["timed_bytes_recv"] / max(xs["timed_steps"], 1),
+                    "wire_ms_per_step": xs["ms_wire"] / max(xs["timed_steps"], 1),
+                    "pack_ms_per_step": xs["ms_pack"] / max(xs["timed_steps"], 1),
+                    "nvlink_gbs": gbs, "peak_gbs": 900.0, "frac": gbs / 900.0,
+                    "peak_source": "NVLink 5 nominal, per direction per GPU",
+                    "note": "diagnostic pass (per-launch events on); min over ranks"}
     stats = {}
     for name in [aug_kernel, "permute", "assign", "pack", "reg_prep", "resize_prep",
                  "resize_pull"]:
@@ -618,6 +637,7 @@ def run_ours(args):
                                        "launches are counted as kernel time",
                              "kernel_only": kernel_only},
                 "storage_roofline": storage,
+                "exchange": exchange,
                 "kernel_ms": {k: (v[1] / v[0] if v[0] else None) for k, v in stats.items()},
                 "cpu_baseline": cpu,
                 "remote_per_epoch": dict(remote_summary(args, n, d, B, totals),

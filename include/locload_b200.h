@@ -231,6 +231,24 @@ int ll_store_insert(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
 int ll_store_gather(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
                     uint8_t* host_dst);
 
+/* ---- distributed consumer: run_training's aggregation (equivalence.cpp:
+ *      121-166) with one learner per process, on caller-owned device buffers
+ *      (e.g. torch tensors), asynchronous on the context's stream ---------- */
+/* grads[i][*] = the toy objective's gradient of sample ids[i] (int64) at w
+ * (equivalence.cpp:52-64); xs[n*dims], ys[n] as ll_toy_synthesize made them */
+int ll_toy_grads_device(ll_ctx* ctx, uintptr_t xs, uintptr_t ys, uint32_t dims, uintptr_t w,
+                        uintptr_t ids, uint64_t n_ids, uintptr_t grads);
+/* out[k] = sum over i of grads[order[i]][k] (order = 0: i), sequentially from
+ * 0.0 -- the deterministic half of the gradient all-reduce: rows gathered
+ * from every rank and summed in ascending sample id (canonical) or per-learner
+ * partials summed in learner order (learner_order) equal the reference's sums
+ * bit for bit (equivalence.cpp:132-148) */
+int ll_ordered_sum_device(ll_ctx* ctx, uintptr_t grads, uint64_t n, uint32_t dims,
+                          uintptr_t order, uintptr_t out);
+/* g = gsum * scale; step_grad = g (if non-zero); w -= lr * g (:157-166) */
+int ll_sgd_apply_device(ll_ctx* ctx, uintptr_t gsum, uint32_t dims, double scale, double lr,
+                        uintptr_t w, uintptr_t step_grad);
+
 /* ---- loader: pipeline.hpp:46-128 ---------------------------------------- */
 typedef struct ll_loader_config {
     uint64_t d;               /* DatasetSpec::n                                 */
@@ -320,6 +338,13 @@ int ll_loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint6
                         uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);
 /* per-epoch totals of the current plan: moved, nvlink-moved, uncached, reg_remote */
 int ll_loader_epoch_totals(ll_loader* ld, uint64_t* out4);
+/* NCCL exchange accounting since the last reset: out8 = {steps, bytes sent,
+ * bytes received (message bytes on the wire), steps timed, bytes received in
+ * the timed steps, ms in the pack kernel, ms from the grouped send/recv's
+ * issue to its completion, 0}; the times cover steps issued while the
+ * context's timing (ll_ctx_set_timing) was on, measured by CUDA events on
+ * the exchange's stream.  NVLink GB/s = timed bytes received / ms on the wire. */
+int ll_loader_exchange_stats(ll_loader* ld, double* out8, int reset);
 
 #ifdef __cplusplus
 }

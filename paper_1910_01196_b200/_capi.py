@@ -135,6 +135,13 @@ PROTOTYPES = {
     "ll_loader_plan_step": (C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, u64p, u64p,
                                       C.POINTER(Move), u32p]),
     "ll_loader_epoch_totals": (C.c_int, [C.c_void_p, u64p]),
+    "ll_loader_exchange_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
+    "ll_toy_grads_device": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_uint32,
+                                      C.c_size_t, C.c_size_t, C.c_uint64, C.c_size_t]),
+    "ll_ordered_sum_device": (C.c_int, [C.c_void_p, C.c_size_t, C.c_uint64, C.c_uint32,
+                                        C.c_size_t, C.c_size_t]),
+    "ll_sgd_apply_device": (C.c_int, [C.c_void_p, C.c_size_t, C.c_uint32, C.c_double,
+                                      C.c_double, C.c_size_t, C.c_size_t]),
     "ll_store_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_uint64]),
     "ll_store_destroy": (C.c_int, [C.c_void_p]),
     "ll_store_size": (C.c_int, [C.c_void_p, u64p]),

@@ -5,6 +5,7 @@
 // implementation and converts exceptions into status codes + ll_last_error().
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -34,6 +35,7 @@ void loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* inf
 void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
                       uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);
 void loader_epoch_totals(ll_loader* ld, uint64_t* out4);
+void loader_exchange_stats(ll_loader* ld, double* out8, int reset);
 // store.cu
 void store_create(ll_store** out, int device, uint64_t capacity_samples);
 void store_destroy(ll_store* st);
@@ -669,6 +671,13 @@ int ll_loader_epoch_totals(ll_loader* ld, uint64_t* out4) {
     return guarded([&] { loader_epoch_totals(ld, out4); });
 }
 
+int ll_loader_exchange_stats(ll_loader* ld, double* out8, int reset) {
+    return guarded([&] {
+        require(ld != nullptr, "null loader");
+        loader_exchange_stats(ld, out8, reset);
+    });
+}
+
 // ---- sample store: SampleCache (pipeline.hpp:68-94) in HBM (store.cu) ----
 int ll_store_create(ll_store** out, int device, uint64_t capacity_samples) {
     return guarded([&] { store_create(out, device, capacity_samples); });
@@ -698,6 +707,38 @@ int ll_store_insert(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
 int ll_store_gather(ll_store* st, ll_ctx* ctx, const uint64_t* ids, uint64_t n,
                     uint8_t* host_dst) {
     return guarded([&] { store_gather(st, ctx, ids, n, host_dst); });
+}
+
+// ---- distributed consumer (one learner per rank), device buffers --------
+int ll_toy_grads_device(ll_ctx* ctx, uintptr_t xs, uintptr_t ys, uint32_t dims, uintptr_t w,
+                        uintptr_t ids, uint64_t n_ids, uintptr_t grads) {
+    return guarded([&] {
+        check_ctx(ctx);
+        require(dims >= 1, "ToyObjective: need n >= 1 and dims >= 1");
+        toy_grads_device(ctx, reinterpret_cast<const double*>(xs),
+                         reinterpret_cast<const double*>(ys), dims,
+                         reinterpret_cast<const double*>(w), reinterpret_cast<const int64_t*>(ids),
+                         n_ids, reinterpret_cast<double*>(grads));
+    });
+}
+
+int ll_ordered_sum_device(ll_ctx* ctx, uintptr_t grads, uint64_t n, uint32_t dims,
+                          uintptr_t order, uintptr_t out) {
+    return guarded([&] {
+        check_ctx(ctx);
+        ordered_sum_device(ctx, reinterpret_cast<const double*>(grads), n, dims,
+                           reinterpret_cast<const int64_t*>(order),
+                           reinterpret_cast<double*>(out));
+    });
+}
+
+int ll_sgd_apply_device(ll_ctx* ctx, uintptr_t gsum, uint32_t dims, double scale, double lr,
+                        uintptr_t w, uintptr_t step_grad) {
+    return guarded([&] {
+        check_ctx(ctx);
+        sgd_apply_device(ctx, reinterpret_cast<const double*>(gsum), dims, scale, lr,
+                         reinterpret_cast<double*>(w), reinterpret_cast<double*>(step_grad));
+    });
 }
 
 } // extern "C"

@@ -7,8 +7,10 @@
 // HBM shard, in move order, into one contiguous send buffer so each move is a
 // single ncclSend (loader.cu issues the grouped send/recv).  Copy-bound:
 // 128-bit loads and streaming stores, one CTA per (sample, 16 KB chunk).
+#include <algorithm>
 #include <vector>
 
+#include "geometry.cuh"
 #include "ll_internal.h"
 
 namespace ll {
@@ -41,6 +43,44 @@ __device__ __forceinline__ void copy_slot(const uint8_t* src, uint8_t* dst, uint
     }
 }
 
+// One sample's resize window into a message slot (resize mode): source rows
+// [y0, y0 + ch) at the sample's pitch, from byte kRecvPad of the slot, as
+// 32-bit copies (word-aligned rows) or bytes.  CTA part of parts.
+__device__ __forceinline__ void copy_resize_window(const uint8_t* sample, uint32_t pitch,
+                                                   uint32_t y0, uint32_t ch, uint8_t* slot,
+                                                   uint32_t part, uint32_t parts) {
+    const uint8_t* s0 = sample + static_cast<uint64_t>(y0) * pitch;
+    uint8_t* d0 = slot + kRecvPad;
+    const uint64_t bytes = static_cast<uint64_t>(ch) * pitch;
+    const uint64_t stride = static_cast<uint64_t>(parts) * blockDim.x;
+    if ((reinterpret_cast<uintptr_t>(s0) & 3) == 0 && (pitch & 3) == 0) {
+        const uint64_t nw = bytes / 4;
+        for (uint64_t c = part * blockDim.x + threadIdx.x; c < nw; c += stride)
+            reinterpret_cast<uint32_t*>(d0)[c] = __ldg(reinterpret_cast<const uint32_t*>(s0) + c);
+    } else {
+        for (uint64_t c = part * blockDim.x + threadIdx.x; c < bytes; c += stride) d0[c] = s0[c];
+    }
+}
+
+// where sample `id` of this learner's shard starts, and its resize window
+__device__ __forceinline__ void resize_source(const ResizeWin& rw, const uint8_t* shard,
+                                              uint64_t shard_first, uint64_t sample_bytes,
+                                              uint64_t id, const uint8_t** sample,
+                                              uint32_t* pitch, uint32_t* y0, uint32_t* ch) {
+    uint32_t H = rw.H, W = rw.W;
+    if (rw.prefix) {
+        var_hw(rw.data_seed, id, &H, &W);
+        *sample = shard + (rw.prefix[id] - rw.prefix[shard_first]);
+        *pitch = var_pitch(W);
+    } else {
+        *sample = shard + (id - shard_first) * sample_bytes;
+        *pitch = 3 * W;
+    }
+    const Params q = aug_params(rw.seed, rw.epoch, id, H, W, rw.out_h, rw.out_w, LL_AUG_RESIZE);
+    *y0 = q.y0;
+    *ch = q.ch;
+}
+
 struct PackArgs {
     const uint32_t* final_step;  // final ids of the step, all learners
     uint32_t n_sends;
@@ -54,6 +94,7 @@ struct PackArgs {
     const uint32_t* aug;
     uint32_t row_bytes;
     uint64_t slot_bytes;
+    ResizeWin rw;
 };
 
 __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
@@ -64,6 +105,15 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
     while (m + 1 < a.n_sends && rem >= a.count[m]) rem -= a.count[m++];
     const uint32_t fi = a.list_first[m] + static_cast<uint32_t>(rem);
     const uint32_t id = a.final_step[fi];
+    if (a.rw.enabled) {
+        const uint8_t* sample;
+        uint32_t pitch, y0, ch;
+        resize_source(a.rw, a.shard, a.shard_first, a.sample_bytes, id, &sample, &pitch, &y0,
+                      &ch);
+        copy_resize_window(sample, pitch, y0, ch, a.out + t * a.slot_bytes,
+                           static_cast<uint32_t>(c), static_cast<uint32_t>(a.chunks));
+        return;
+    }
     const uint8_t* src = a.shard + (id - a.shard_first) * a.sample_bytes;
     copy_slot(src, a.out + t * a.slot_bytes, a.sample_bytes, a.aug != nullptr,
               a.aug ? a.aug[fi] : 0u, a.row_bytes, static_cast<uint32_t>(c),
@@ -102,7 +152,7 @@ __global__ void __launch_bounds__(256) k_reg_prep(RegPrepArgs a) {
     const uint32_t o = v >> 24;
     if (j != a.me && o != a.me) return;  // neither mine to send nor in my slice
     __shared__ uint32_t s_rank;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && o < a.p) {
         uint32_t before = 0;
         for (uint32_t jj = 0; jj < j; ++jj) before += a.regcnt[jj * a.p + o];
         s_rank = (v & 0xFFFFFFu) - before;
@@ -110,9 +160,11 @@ __global__ void __launch_bounds__(256) k_reg_prep(RegPrepArgs a) {
     __syncthreads();
     const uint32_t rank = s_rank;
     if (j == a.me) {
-        if (threadIdx.x == 0) a.ridx[e - j * a.L] = o == a.me ? kLocal : o * a.L + rank;
+        // own samples and uncached ones (o == p: the storage tier) are not received
+        if (threadIdx.x == 0) a.ridx[e - j * a.L] = o == a.me || o >= a.p ? kLocal : o * a.L + rank;
         return;
     }
+    if (o >= a.p) return;  // uncached: every learner reads it from the storage tier
     // o == me, j != me: copy the sample into message (j), slot rank
     const uint32_t id = a.batch[e];
     copy_slot(a.shard + (id - a.shard_first) * a.sample_bytes,
@@ -136,9 +188,16 @@ void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scr
     });
 }
 
+uint64_t resize_slot_bytes(bool variable, uint32_t H, uint32_t W) {
+    const uint64_t side = variable ? kVarMin + kVarSpan - 1 : std::min(H, W);
+    const uint64_t pitch = variable ? var_pitch(kVarMin + kVarSpan - 1) : 3ull * W;
+    return pad16(side * pitch) + kRecvPad + 64;  // + K7's read slack past a window row
+}
+
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
-                 uint8_t* packbuf, const uint32_t* d_aug, uint32_t row_bytes) {
+                 uint8_t* packbuf, const uint32_t* d_aug, uint32_t row_bytes,
+                 const ResizeWin& rw) {
     PackArgs a{};
     uint64_t n_pack = 0;
     for (const ll_xfer& x : xfers) {
@@ -149,12 +208,14 @@ void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t*
         n_pack += x.count;
     }
     if (n_pack == 0) return;
-    require(sample_bytes % 16 == 0, "exchange: sample bytes must be a multiple of 16");
+    require(rw.enabled || sample_bytes % 16 == 0,
+            "exchange: sample bytes must be a multiple of 16");
     a.final_step = d_final_step;
     a.shard = shard;
     a.shard_first = shard_first;
     a.sample_bytes = sample_bytes;
-    a.slot_bytes = d_aug ? kWinBytes : sample_bytes;
+    a.rw = rw;
+    a.slot_bytes = rw.enabled ? rw.slot : d_aug ? kWinBytes : sample_bytes;
     a.chunks = (a.slot_bytes + kChunk - 1) / kChunk;
     a.out = packbuf;
     a.aug = d_aug;

@@ -225,7 +225,12 @@ struct SrcMap {
     // NCCL receive slots hold crop windows (kWinRows rows at recv_row pitch,
     // from the 16-byte-aligned window start) when recv_row != 0, else samples
     uint32_t recv_row = 0;
+    // resize mode over NCCL: slots of recv_slot bytes, each holding a sample's
+    // resize window -- its source rows [y0, y0 + ch) at the sample's pitch,
+    // from byte kRecvPad of the slot (0: slots hold whole samples)
+    uint64_t recv_slot = 0;
 };
+constexpr uint32_t kRecvPad = 16;
 // NCCL messages carry a crop-mode sample as its crop window only: 224 rows of
 // the 16-byte-aligned span holding its 672 window bytes (<= 704 bytes), not
 // the whole 196,608-byte sample
@@ -263,15 +268,35 @@ void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scr
                      const uint32_t* d_regcnt, uint32_t p, uint32_t me, uint64_t B,
                      const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
                      uint8_t* pack, uint32_t* ridx, const uint32_t* d_aug, uint32_t row_bytes);
+// resize-mode messages: each slot carries the sample's resize window (rows
+// [y0, y0 + ch) at its pitch, from byte kRecvPad); the geometry and crop
+// origin come from the id, as in K7's prologue
+struct ResizeWin {
+    bool enabled = false;
+    uint64_t seed = 0, epoch = 0, data_seed = 0;
+    const uint64_t* prefix = nullptr;  // variable geometry (else fixed H x W)
+    uint32_t H = 0, W = 0, out_h = 0, out_w = 0;
+    uint64_t slot = 0;                 // message slot bytes
+};
+// the largest resize window (+ pad and tail slack), per message slot
+uint64_t resize_slot_bytes(bool variable, uint32_t H, uint32_t W);
+// sends: (list_first, count) runs of the step's final ids, packed contiguously
 void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t* d_final_step,
                  const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
-                 uint8_t* packbuf, const uint32_t* d_aug, uint32_t row_bytes);
+                 uint8_t* packbuf, const uint32_t* d_aug, uint32_t row_bytes,
+                 const ResizeWin& rw = ResizeWin());
 
 // train.cu: consumer side (equivalence.cpp:95-205) on the device
 void train_run_device(ll_ctx* ctx, const double* h_xs, const double* h_ys, uint64_t n,
                       uint32_t dims, int scheme, uint32_t p, uint64_t B, uint64_t steps,
                       uint64_t seed, double lr, int aggregation, double* h_final_w,
                       double* h_step_grads);
+void toy_grads_device(ll_ctx* ctx, const double* X, const double* Y, uint32_t dims,
+                      const double* w, const int64_t* ids, uint64_t n_ids, double* G);
+void ordered_sum_device(ll_ctx* ctx, const double* G, uint64_t n, uint32_t dims,
+                        const int64_t* order, double* out);
+void sgd_apply_device(ll_ctx* ctx, const double* gsum, uint32_t dims, double scale, double lr,
+                      double* w, double* step_grad);
 void full_batch_gradient_device(ll_ctx* ctx, const double* h_xs, const double* h_ys, uint64_t n,
                                 uint32_t dims, const double* h_w, const uint64_t* h_batch,
                                 uint64_t B, double* h_grad);

@@ -131,6 +131,15 @@ struct ll_loader {
     std::vector<std::unique_ptr<HostSlot>> hslots;
     uint64_t submitted = 0, waited = 0;
     cudaStream_t side = nullptr;     // prologue stream of host-driven steps
+    // NCCL exchange accounting: bytes every step; with the context's timing
+    // on, events around each step's pack and wire phase on its stream
+    struct XTimes {
+        cudaEvent_t t0, t1, t2;
+        uint64_t recvd;
+    };
+    std::vector<XTimes> xtimes;
+    uint64_t x_steps = 0, x_sent = 0, x_recv = 0, x_timed = 0, x_timed_recv = 0;
+    double x_ms_pack = 0, x_ms_wire = 0;
 };
 
 namespace ll {
@@ -225,23 +234,67 @@ void ensure_out(ll_loader* ld) {
 //  * regular scheme (reg_slice, sampling.cpp:27-42): every learner exchanges
 //    with every other its owned samples of their slices (h_regcnt: this
 //    step's [slice][owner] counts); x.ridx maps slice positions to x.recv.
-void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_move* h_moves,
-                    uint32_t h_nmoves, const uint32_t* h_off, const uint32_t* h_regcnt,
-                    ll_loader::ExSet& x, cudaStream_t stream) {
+// Brackets one step's exchange on its stream: pack kernel (t0 -> t1) and
+// NCCL grouped send/recv (t1 -> t2), while the context's timing is on.
+struct ExchangeTimer {
+    ll_loader* ld;
+    cudaStream_t stream;
+    ll_loader::XTimes t{nullptr, nullptr, nullptr, 0};
+    ExchangeTimer(ll_loader* l, cudaStream_t s) : ld(l), stream(s) {
+        if (!ld->ctx->timing) return;
+        t.t0 = ld->ctx->take_event();
+        LL_CUDA(cudaEventRecord(t.t0, stream));
+    }
+    void packed() {
+        if (!t.t0) return;
+        t.t1 = ld->ctx->take_event();
+        LL_CUDA(cudaEventRecord(t.t1, stream));
+    }
+    void done(uint64_t sent, uint64_t recvd) {
+        ++ld->x_steps;
+        ld->x_sent += sent;
+        ld->x_recv += recvd;
+        if (!t.t0) return;
+        t.t2 = ld->ctx->take_event();
+        LL_CUDA(cudaEventRecord(t.t2, stream));
+        t.recvd = recvd;
+        ld->xtimes.push_back(t);
+        t = ll_loader::XTimes{nullptr, nullptr, nullptr, 0};  // owned by xtimes now
+    }
+    ~ExchangeTimer() {  // an exception before done(): hand the events back
+        for (cudaEvent_t e : {t.t0, t.t1, t.t2})
+            if (e) ld->ctx->event_pool.push_back(e);
+    }
+};
+
+// Bytes per NCCL message slot: a crop window (crop mode) or the largest
+// resize window (resize mode, rows at the sample's pitch after kRecvPad).
+uint64_t msg_slot(const ll_loader* ld) {
+    const ll_loader_config& c = ld->cfg;
+    if (c.augment.mode == LL_AUG_CROP) return kWinBytes;
+    return resize_slot_bytes(c.geometry == LL_GEOM_VARIABLE, c.height, c.width);
+}
+
+void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t step,
+                    const ll_move* h_moves, uint32_t h_nmoves, const uint32_t* h_off,
+                    const uint32_t* h_regcnt, ll_loader::ExSet& x, cudaStream_t stream) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
     const uint64_t B = c.batch_size;
     require(ld->comm != nullptr, "loader: NCCL exchange needs ll_loader_comm_init");
-    require(c.geometry == LL_GEOM_FIXED, "loader: variable-size samples need the P2P exchange");
     const uint32_t* d_final_step = pd.final_ids + step * B;
     cudaStream_t main = ctx->stream;
-    // crop mode: messages carry crop windows (K6 reads nothing else of a sample)
-    const bool win = c.augment.mode == LL_AUG_CROP;
-    const uint64_t slot = win ? kWinBytes : ld->S;
-    const uint32_t* d_aug = win ? pd.aug + step * B : nullptr;
+    // crop mode: messages carry crop windows (K6 reads nothing else of a
+    // sample); resize mode: resize windows (K7 reads nothing else)
+    const bool crop = c.augment.mode == LL_AUG_CROP;
+    const uint64_t slot = msg_slot(ld);
+    const uint32_t* d_aug = crop ? pd.aug + step * B : nullptr;
     const uint32_t row_bytes = 3 * c.width;
+    ExchangeTimer tm(ld, stream);
     if (c.scheme == LL_SCHEME_REGULAR) {
+        require(crop, "loader: the regular scheme over NCCL needs crop mode (resize windows of "
+                      "a full slice exchange go over the P2P exchange)");
         require(h_regcnt != nullptr && pd.regcnt != nullptr, "loader: regular plan lacks counts");
         const uint64_t L = B / p;
         x.pack.need(B * slot, "exchange send buffer");
@@ -257,6 +310,8 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
             throw;
         }
         ctx->stream = main;
+        tm.packed();
+        uint64_t sent = 0, recvd = 0;
         LL_NCCL(ncclGroupStart());
         for (uint32_t r = 0; r < p; ++r) {
             if (r == me) continue;
@@ -267,34 +322,75 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_mo
             if (nr)
                 LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + r * L * slot, nr * slot, ncclUint8,
                                  static_cast<int>(r), ld->comm, stream));
+            sent += ns * slot;
+            recvd += nr * slot;
         }
         LL_NCCL(ncclGroupEnd());
+        tm.done(sent, recvd);
         return;
     }
-    const std::vector<ll_xfer> xs = exchange_plan(h_moves, h_nmoves, h_off, me);
-    uint64_t n_send = 0, n_recv = 0;
-    for (const ll_xfer& xf : xs) (xf.is_send ? n_send : n_recv) += xf.count;
-    x.pack.need(n_send * slot, "exchange send buffer");
-    x.recv.need(n_recv * slot, "exchange receive buffer");
+    // balanced / locality schemes: one message per tail move involving me
+    // (equivalence.cpp:77-88).  A run hands the sender's cached samples over
+    // first and its uncached ones (storage tier, alpha < 1) last, so only the
+    // run's first `nvlink` samples cross the wire; the receive slots stay
+    // indexed by whole runs (slot = final-list position - kept), and K6 / K7
+    // read uncached samples from the storage tier.
+    std::vector<ll_xfer> xs;
+    uint64_t so = 0, ro = 0;
+    for (uint32_t m = 0; m < h_nmoves; ++m) {
+        const ll_move& mv = h_moves[m];
+        if (mv.sender == me) {
+            xs.push_back(ll_xfer{mv.receiver, 1, mv.nvlink, so,
+                                 static_cast<uint64_t>(h_off[mv.receiver]) + mv.dst_off});
+            so += mv.nvlink;
+        }
+        if (mv.receiver == me) {
+            xs.push_back(ll_xfer{mv.sender, 0, mv.nvlink, ro,
+                                 static_cast<uint64_t>(h_off[me]) + mv.dst_off});
+            ro += mv.count;
+        }
+    }
+    x.pack.need(so * slot, "exchange send buffer");
+    x.recv.need(ro * slot, "exchange receive buffer");
+    ResizeWin rw;
+    if (!crop) {
+        rw.enabled = true;
+        rw.seed = c.seed;
+        rw.epoch = epoch;
+        rw.data_seed = c.data_seed;
+        rw.prefix = c.geometry == LL_GEOM_VARIABLE ? ld->prefix.as<uint64_t>() : nullptr;
+        rw.H = c.height;
+        rw.W = c.width;
+        rw.out_h = c.augment.out_h;
+        rw.out_w = c.augment.out_w;
+        rw.slot = slot;
+    }
     ctx->stream = stream;  // pack_device launches on the context stream
     try {
         pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
-                    x.pack.as<uint8_t>(), d_aug, row_bytes);
+                    x.pack.as<uint8_t>(), d_aug, row_bytes, rw);
     } catch (...) {
         ctx->stream = main;
         throw;
     }
     ctx->stream = main;
+    tm.packed();
+    uint64_t sent = 0, recvd = 0;
     LL_NCCL(ncclGroupStart());
     for (const ll_xfer& xf : xs) {
-        if (xf.is_send)
+        if (xf.count == 0) continue;
+        if (xf.is_send) {
             LL_NCCL(ncclSend(x.pack.as<uint8_t>() + xf.buf_first * slot, xf.count * slot,
                              ncclUint8, static_cast<int>(xf.peer), ld->comm, stream));
-        else
+            sent += xf.count * slot;
+        } else {
             LL_NCCL(ncclRecv(x.recv.as<uint8_t>() + xf.buf_first * slot, xf.count * slot,
                              ncclUint8, static_cast<int>(xf.peer), ld->comm, stream));
+            recvd += xf.count * slot;
+        }
     }
     LL_NCCL(ncclGroupEnd());
+    tm.done(sent, recvd);
 }
 
 // Where this learner's samples of `step` come from (own shard, storage tier,
@@ -383,10 +479,16 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
         const ll_loader::ExSet* x = prefetched;
         require(x != nullptr, "loader: NCCL step without an issued exchange");
         src.recv = x->recv.as<uint8_t>();
-        if (c.augment.mode == LL_AUG_CROP) src.recv_row = kWinRow;  // window slots
+        if (c.augment.mode == LL_AUG_CROP)
+            src.recv_row = kWinRow;  // crop-window slots
+        else
+            src.recv_slot = msg_slot(ld);  // resize-window slots
         if (reg) {
             src.recv_idx = x->ridx.as<uint32_t>();
-            n_recv = nvl_recv = n_local - h_regcnt[me * p + me];
+            n_recv = nvl_recv = 0;  // this slice's samples owned by the others
+            for (uint32_t o = 0; o < p; ++o)
+                if (o != me) n_recv += h_regcnt[me * p + o];
+            nvl_recv = n_recv;
         }
     }
     ensure_out(ld);
@@ -401,7 +503,10 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
         info->kept = src.kept;
         info->received = n_recv;
         info->moved_total = h_stats[0];
-        info->nvlink_bytes = nvl_recv * ld->S;
+        // bytes that crossed NVLink into this learner: NCCL message slots, or
+        // (P2P) the samples' bytes read from peer shards
+        info->nvlink_bytes =
+            nvl_recv * (p > 1 && c.exchange == LL_EXCHANGE_NCCL ? msg_slot(ld) : ld->S);
         info->uncached = h_stats[2];
         info->reg_remote = h_stats[3] == 0xFFFFFFFFu ? UINT64_MAX : h_stats[3];
         info->device_out = reinterpret_cast<uintptr_t>(out);
@@ -519,8 +624,8 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
     if (ld->cached < c.d) {
         require(c.geometry == LL_GEOM_FIXED,
                 "Loader: the storage tier (alpha < 1) supports fixed-size samples");
-        require(c.learners == 1 || c.exchange == LL_EXCHANGE_P2P,
-                "Loader: the storage tier (alpha < 1) needs the P2P exchange");
+        require(c.learners == 1 || c.exchange != LL_EXCHANGE_NONE,
+                "Loader: the storage tier (alpha < 1) with several learners needs an exchange");
     }
     const uint64_t p = c.learners, j = c.rank;
     ld->first = (j * ld->cached + p - 1) / p;
@@ -543,8 +648,8 @@ void loader_create(ll_loader** out, ll_ctx* ctx, const ll_loader_config* cfg) {
         ld->h_prefix_ends.assign(ends, ends + 2);
         shard_bytes = ends[1] - ends[0];
     }
-    // + 16: K7's word-aligned taps read up to 8 bytes past a row's last pixel
-    ld->shard.reserve(std::max<uint64_t>(shard_bytes, 16) + 16);
+    // + 64: K7 reads up to 27 bytes past a crop row (word-aligned taps, TMA spans)
+    ld->shard.reserve(std::max<uint64_t>(shard_bytes, 16) + 64);
     for (auto& sl : ld->slot) {
         sl.order.reserve(sizeof(uint32_t) * c.d);
         sl.plan.reserve(ld->steps, c.batch_size);
@@ -614,9 +719,14 @@ void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     const uint64_t share = (B + p - 1) / p;
     // the message slot issue_exchange uses: a crop window (which may exceed a
     // small source's whole sample, e.g. 224 x 224) or the whole sample
-    const uint64_t slot = c.augment.mode == LL_AUG_CROP ? kWinBytes : ld->S;
+    const uint64_t slot = msg_slot(ld);
+    // sends: at most the batch in crop mode; resize slots are large (a whole
+    // resize window), so there a learner's sends are capped at its share --
+    // a learner sends count - target <= B - B/p, which exceeds B/p only when
+    // it owns over half of a p > 2 batch (need() fails loudly if it ever does)
+    const uint64_t max_send = c.augment.mode == LL_AUG_CROP ? B : share;
     for (ll_loader::ExSet* x : {&ld->xset[0], &ld->xset[1]}) {
-        x->pack.reserve(std::max<uint64_t>(B * slot, 16));
+        x->pack.reserve(std::max<uint64_t>(max_send * slot, 16));
         x->recv.reserve(std::max<uint64_t>((c.scheme == LL_SCHEME_REGULAR ? B : share) * slot, 16));
         x->ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(share, 1));
     }
@@ -1007,7 +1117,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             auto [mv, off, kept, nm, st] = tables(step);
             (void)kept;
             (void)st;
-            issue_exchange(ld, ld->plan().view(), step, mv, nm, off, regcnt(step),
+            issue_exchange(ld, ld->plan().view(), epoch, step, mv, nm, off, regcnt(step),
                            ld->xset[slot], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[slot], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
@@ -1083,7 +1193,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             auto [mv, off, kept, nm, st] = tables(step + 1);
             (void)kept;
             (void)st;
-            issue_exchange(ld, ld->plan().view(), step + 1, mv, nm, off, regcnt(step + 1),
+            issue_exchange(ld, ld->plan().view(), epoch, step + 1, mv, nm, off, regcnt(step + 1),
                            ld->xset[ns], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[ns], ld->side));
             ld->xpending[ns] = {true, epoch, step + 1};
@@ -1227,7 +1337,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[xs], 0));
             // a loader_step prefetch parked in this set is clobbered now
             ld->xpending[xs].valid = false;
-            issue_exchange(ld, pd, 0, t->moves, t->n, t->off, rc, ld->xset[xs], ld->side);
+            issue_exchange(ld, pd, epoch, 0, t->moves, t->n, t->off, rc, ld->xset[xs], ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[xs], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[xs], 0));
             pre = &ld->xset[xs];
@@ -1309,6 +1419,36 @@ void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_
     }
     *n_moves = ld->h_nmoves[step];
     for (uint32_t m = 0; m < *n_moves; ++m) moves[m] = ld->h_moves[step * kMaxP + m];
+}
+
+// {steps, bytes sent, bytes received, timed steps, bytes received in timed
+// steps, ms packing, ms on the wire, 0}
+void loader_exchange_stats(ll_loader* ld, double* out8, int reset) {
+    set_device(ld->ctx);
+    for (const auto& t : ld->xtimes) {
+        LL_CUDA(cudaEventSynchronize(t.t2));
+        float a = 0, b = 0;
+        LL_CUDA(cudaEventElapsedTime(&a, t.t0, t.t1));
+        LL_CUDA(cudaEventElapsedTime(&b, t.t1, t.t2));
+        ld->x_ms_pack += a;
+        ld->x_ms_wire += b;
+        ++ld->x_timed;
+        ld->x_timed_recv += t.recvd;
+        for (cudaEvent_t e : {t.t0, t.t1, t.t2}) ld->ctx->event_pool.push_back(e);
+    }
+    ld->xtimes.clear();
+    out8[0] = static_cast<double>(ld->x_steps);
+    out8[1] = static_cast<double>(ld->x_sent);
+    out8[2] = static_cast<double>(ld->x_recv);
+    out8[3] = static_cast<double>(ld->x_timed);
+    out8[4] = static_cast<double>(ld->x_timed_recv);
+    out8[5] = ld->x_ms_pack;
+    out8[6] = ld->x_ms_wire;
+    out8[7] = 0;
+    if (reset) {
+        ld->x_steps = ld->x_sent = ld->x_recv = ld->x_timed = ld->x_timed_recv = 0;
+        ld->x_ms_pack = ld->x_ms_wire = 0;
+    }
 }
 
 void loader_epoch_totals(ll_loader* ld, uint64_t* out4) {

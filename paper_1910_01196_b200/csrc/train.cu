@@ -22,9 +22,10 @@ namespace ll {
 namespace {
 
 // G[i][k] = (dot(w, x_s) - y_s) * x_s[k] for s = ids[i]  (equivalence.cpp:52-64)
+template <typename Id>
 __global__ void k_sample_grads(const double* __restrict__ X, const double* __restrict__ Y,
                                uint32_t dims, const double* __restrict__ w,
-                               const uint32_t* __restrict__ ids, uint64_t n_ids,
+                               const Id* __restrict__ ids, uint64_t n_ids,
                                double* __restrict__ G) {
     const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
     if (i >= n_ids) return;
@@ -58,6 +59,32 @@ __global__ void k_aggregate_update(const double* __restrict__ G, uint64_t n_ids,
         }
     }
     g = __dmul_rn(g, scale);
+    if (step_grad) step_grad[k] = g;
+    w[k] = __dsub_rn(w[k], __dmul_rn(lr, g));
+}
+
+// out[k] = sum over i of G[order[i]][k] (order == nullptr: i itself),
+// sequentially from 0.0 in that order -- the reference's summation order,
+// so a sum split across learners and put back together in the same order is
+// bit-identical (equivalence.cpp:132-148).  One thread per coordinate.
+__global__ void k_ordered_sum(const double* __restrict__ G, uint64_t n, uint32_t dims,
+                              const int64_t* __restrict__ order, double* __restrict__ out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= dims) return;
+    double g = 0.0;
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t r = order ? static_cast<uint64_t>(order[i]) : i;
+        g = __dadd_rn(g, G[r * dims + k]);
+    }
+    out[k] = g;
+}
+
+// g *= scale (1/B), step_grad = g, w -= lr * g  (equivalence.cpp:157-166)
+__global__ void k_sgd_apply(const double* __restrict__ gsum, uint32_t dims, double scale,
+                            double lr, double* __restrict__ w, double* __restrict__ step_grad) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= dims) return;
+    const double g = __dmul_rn(gsum[k], scale);
     if (step_grad) step_grad[k] = g;
     w[k] = __dsub_rn(w[k], __dmul_rn(lr, g));
 }
@@ -133,7 +160,7 @@ void train_run_device(ll_ctx* ctx, const double* h_xs, const double* h_ys, uint6
                                         : plan->view().final_ids + st * B;
         const uint32_t* off = canonical ? nullptr : plan->view().off + st * (kMaxP + 1);
         launch(ctx, "train_grads", [&] {
-            k_sample_grads<<<blocks(B, 128), 128, 0, ctx->stream>>>(
+            k_sample_grads<uint32_t><<<blocks(B, 128), 128, 0, ctx->stream>>>(
                 X.as<double>(), Y.as<double>(), dims, W.as<double>(), ids, B, G.as<double>());
         });
         launch(ctx, "train_update", [&] {
@@ -169,7 +196,7 @@ void full_batch_gradient_device(ll_ctx* ctx, const double* h_xs, const double* h
                             ctx->stream));
     narrow_device(ctx, ids64.as<uint64_t>(), ids.as<uint32_t>(), B);
     launch(ctx, "train_grads", [&] {
-        k_sample_grads<<<blocks(B, 128), 128, 0, ctx->stream>>>(
+        k_sample_grads<uint32_t><<<blocks(B, 128), 128, 0, ctx->stream>>>(
             X.as<double>(), Y.as<double>(), dims, W.as<double>(), ids.as<uint32_t>(), B,
             G.as<double>());
     });
@@ -183,6 +210,32 @@ void full_batch_gradient_device(ll_ctx* ctx, const double* h_xs, const double* h
     LL_CUDA(cudaMemcpyAsync(h_grad, SG.ptr, sizeof(double) * dims, cudaMemcpyDeviceToHost,
                             ctx->stream));
     LL_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ---- consumer steps on caller-owned device buffers (one learner per rank) --
+void toy_grads_device(ll_ctx* ctx, const double* X, const double* Y, uint32_t dims,
+                      const double* w, const int64_t* ids, uint64_t n_ids, double* G) {
+    if (n_ids == 0) return;
+    launch(ctx, "train_grads", [&] {
+        k_sample_grads<int64_t><<<blocks(n_ids, 128), 128, 0, ctx->stream>>>(X, Y, dims, w, ids,
+                                                                             n_ids, G);
+    });
+}
+
+void ordered_sum_device(ll_ctx* ctx, const double* G, uint64_t n, uint32_t dims,
+                        const int64_t* order, double* out) {
+    const unsigned t = dims < 128 ? 32 * ((dims + 31) / 32) : 128;
+    launch(ctx, "ordered_sum", [&] {
+        k_ordered_sum<<<blocks(dims, t), t, 0, ctx->stream>>>(G, n, dims, order, out);
+    });
+}
+
+void sgd_apply_device(ll_ctx* ctx, const double* gsum, uint32_t dims, double scale, double lr,
+                      double* w, double* step_grad) {
+    const unsigned t = dims < 128 ? 32 * ((dims + 31) / 32) : 128;
+    launch(ctx, "sgd_apply", [&] {
+        k_sgd_apply<<<blocks(dims, t), t, 0, ctx->stream>>>(gsum, dims, scale, lr, w, step_grad);
+    });
 }
 
 } // namespace ll

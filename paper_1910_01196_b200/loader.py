@@ -224,6 +224,17 @@ class DeviceLoader:
         return {"moved": int(out[0]), "moved_nvlink": int(out[1]), "uncached": int(out[2]),
                 "reg_remote": int(out[3])}
 
+    def exchange_stats(self, reset: bool = False) -> dict:
+        """NCCL exchange accounting (ll_loader_exchange_stats)."""
+        out = (C.c_double * 8)()
+        check(_capi.lib().ll_loader_exchange_stats(self._h, out, 1 if reset else 0))
+        r = {"steps": int(out[0]), "bytes_sent": int(out[1]), "bytes_recv": int(out[2]),
+             "timed_steps": int(out[3]), "timed_bytes_recv": int(out[4]), "ms_pack": out[5],
+             "ms_wire": out[6]}
+        r["wire_gbs"] = (r["timed_bytes_recv"] / (r["ms_wire"] / 1e3) / 1e9
+                         if r["ms_wire"] > 0 else None)
+        return r
+
     def fetch(self, info: _capi.StepInfo) -> np.ndarray:
         """Host copy of a step's augmented batch [n_local, 3, out_h, out_w]
         (bf16 comes back as raw uint16 bits)."""

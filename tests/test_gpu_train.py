@@ -75,3 +75,21 @@ def test_errors_match_reference():
         ll.run_training(obj, "regular", 5, 12, 10, 6, 0.01)
     with pytest.raises(ValueError):
         oracle.ref_run_training(120, 8, 5, "regular", 5, 12, 10, 6, 0.01)
+
+
+@pytest.mark.parametrize("agg", ["canonical", "learner_order", "allreduce"])
+@pytest.mark.parametrize("scheme", ["regular", "locality", "locality_balanced"])
+def test_distributed_trainer_device_ops_bit_exact(scheme, agg):
+    """train_dist.DistributedTrainer on one process (all learners local): lists
+    from ll_plan_epoch, per-sample gradients (ll_toy_grads_device), ordered
+    sums (ll_ordered_sum_device) and the update (ll_sgd_apply_device) on the
+    GPU.  With one process the all-reduce is the learner-order sum, so every
+    aggregation must equal the reference bit for bit."""
+    from paper_1910_01196_b200.train_dist import DistributedTrainer
+    n, dims, os_, p, B, steps, seed, lr = 512, 8, 21, 4, 64, 20, 2, 0.01
+    obj = ll.ToyObjective.synthesize(n, dims, os_)
+    run = DistributedTrainer(obj, scheme, p, B, seed, lr, aggregation=agg).run(steps)
+    ref_agg = "canonical" if agg == "canonical" else "learner_order"
+    w, g = oracle.ref_run_training(n, dims, os_, scheme, p, B, steps, seed, lr, ref_agg)
+    assert np.array_equal(run.final_weights, w), (scheme, agg)
+    assert np.array_equal(run.step_gradients, g), (scheme, agg)
