@@ -711,186 +711,6 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
     }
 }
 
-// K7 staged: the band's source rows come into shared memory by TMA bulk
-// copies (one cp.async.bulk per row, issued by the lanes of warp 0 and
-// completing on one mbarrier), and the taps read them with LDS instead of
-// L1/L2 gathers.  Row i of the smem band is source row ylo(first output row)
-// + i; it holds the crop span from the 16-byte-aligned address below the
-// crop start, so the tap word of a column is (row word base) + (column word
-// offset) with a per-column byte phase (the row pitch is a multiple of 4).
-// The copy engine moves the bytes, so the compute warps issue no staging
-// instructions; their per-column setup overlaps the copies.
-constexpr uint32_t kStageStride = 3 * (kVarMin + kVarSpan - 1) + 32;  // 1568: span + phase + tail
-static_assert(kStageStride % 16 == 0, "TMA destinations are 16-byte aligned");
-
-__host__ __device__ constexpr uint32_t staged_rows_max(uint32_t rb, uint32_t max_side,
-                                                       uint32_t out_h) {
-    return ((rb - 1) * max_side + out_h - 1) / out_h + 3;
-}
-
-__device__ __forceinline__ void row_taps_s(uint32_t saddr, uint32_t sel, uint32_t* rg,
-                                           uint32_t* bb) {
-    uint32_t w0, w1, w2;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w0) : "r"(saddr));
-    asm volatile("ld.shared.u32 %0, [%1+4];" : "=r"(w1) : "r"(saddr));
-    asm volatile("ld.shared.u32 %0, [%1+8];" : "=r"(w2) : "r"(saddr));
-    const uint32_t ta = f4e(w0, w1, sel), tb = f4e(w1, w2, sel);  // [Ra Ga Ba Rb] [Gb Bb - -]
-    *rg = __byte_perm(ta, tb, 0x4130);
-    *bb = __byte_perm(ta, tb, 0x0052);
-}
-
-template <bool BF16, uint32_t RB, uint32_t OUT = 0>
-__global__ void __launch_bounds__(kMaxOutW) k_augment_resize_staged(AugArgs a,
-                                                                    const ResizeItem* items,
-                                                                    uint32_t rows_cap) {
-    extern __shared__ __align__(16) uint8_t s_band[];
-    __shared__ uint4 s_row[RB];  // {lo row word base, hi row word base, 128-wy, wy}
-    __shared__ Params s_q;
-    __shared__ uint32_t s_ph4, s_nrows;
-    __shared__ __align__(8) uint64_t s_mbar;
-    const uint64_t k = blockIdx.x;
-    const uint32_t oy0 = blockIdx.y * RB;
-    const uint32_t rows_out = a.out_h - oy0 < RB ? a.out_h - oy0 : RB;
-    const uint32_t tid = threadIdx.x;
-    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(s_band));
-    const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
-    const ResizeItem it = items[k];
-    uint32_t yfirst;
-    {
-        uint32_t w;
-        resize_tap<uint32_t>(oy0, a.out_h, it.q.ch, &yfirst, &w);
-    }
-    if (tid < rows_out) {
-        uint32_t ylo, wy;
-        resize_tap<uint32_t>(oy0 + tid, a.out_h, it.q.ch, &ylo, &wy);
-        const uint32_t yhi = wy ? ylo + 1 : ylo;
-        // row i starts at i * stride + phase_i, phase_i = its crop start mod
-        // 16; word base = that minus the sample-constant phase mod 4
-        auto word_base = [&](uint32_t y) -> uint32_t {
-            const uintptr_t st = reinterpret_cast<uintptr_t>(it.src) +
-                                 static_cast<uintptr_t>(it.q.y0 + y) * it.pitch + 3 * it.q.x0;
-            return (y - yfirst) * kStageStride + (static_cast<uint32_t>(st) & 12u);
-        };
-        s_row[tid] = make_uint4(word_base(ylo), word_base(yhi), 128 - wy, wy);
-        if (tid == rows_out - 1) {
-            const uint32_t n = yhi - yfirst + 1;
-            s_nrows = n <= rows_cap ? n : 0;  // 0: over the smem sizing (host bug)
-        }
-        if (tid == 0) {
-            s_q = it.q;
-            s_ph4 = static_cast<uint32_t>(reinterpret_cast<uintptr_t>(it.src) + 3 * it.q.x0) & 3u;
-            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-    }
-    __syncthreads();
-    const Params q = s_q;
-    const uint32_t nrows = s_nrows;
-    if (nrows == 0) __trap();
-    if (tid < 32) {
-        // warp 0: the band rows as bulk copies, one row per lane (and lane + 32)
-        const uint32_t span = 3 * q.cw + 12;  // taps read up to 3 words past a pixel
-        uint32_t my_bytes = 0;
-        for (uint32_t i = tid; i < nrows; i += 32) {
-            const uintptr_t st = reinterpret_cast<uintptr_t>(it.src) +
-                                 static_cast<uintptr_t>(q.y0 + yfirst + i) * it.pitch + 3 * q.x0;
-            const uint32_t ph = static_cast<uint32_t>(st) & 15u;
-            my_bytes += (ph + span + 15u) & ~15u;
-        }
-        uint32_t total = my_bytes;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-        if (tid == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
-                         "r"(total)
-                         : "memory");
-        __syncwarp();
-        for (uint32_t i = tid; i < nrows; i += 32) {
-            const uintptr_t st = reinterpret_cast<uintptr_t>(it.src) +
-                                 static_cast<uintptr_t>(q.y0 + yfirst + i) * it.pitch + 3 * q.x0;
-            const uint32_t ph = static_cast<uint32_t>(st) & 15u;
-            const uint32_t bytes = (ph + span + 15u) & ~15u;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    sbase + i * kStageStride),
-                "l"(st - ph), "r"(bytes), "r"(mb)
-                : "memory");
-        }
-    }
-    // per-column constants while the rows are in flight
-    const uint32_t ox = tid < a.out_w ? tid : a.out_w - 1;
-    uint32_t xlo, wx;
-    resize_tap<uint32_t>(q.flip ? a.out_w - 1 - ox : ox, a.out_w, q.cw, &xlo, &wx);
-    uint32_t x3 = 3 * xlo, colw = (128 - wx) | (wx << 16);
-    if (wx == 0 && xlo > 0) {  // taps (xlo-1, xlo) weighted (0, 128): no read past xlo
-        x3 -= 3;
-        colw = 128u << 16;
-    }
-    const uint32_t colb = s_ph4 + x3;
-    const uint32_t colword = sbase + (colb & ~3u), sel = colb & 3u;
-    uint64_t mean2[3], inv2[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        mean2[c] = pk(__float_as_uint(a.nc.mean255[c]), __float_as_uint(a.nc.mean255[c]));
-        inv2[c] = pk(__float_as_uint(a.nc.inv_std255[c]), __float_as_uint(a.nc.inv_std255[c]));
-    }
-    {
-        uint32_t done = 0;
-        while (!done) {
-            asm volatile(
-                "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
-                : "=r"(done)
-                : "r"(mb)
-                : "memory");
-        }
-    }
-    if (tid >= a.out_w) return;
-    const uint64_t k512 = 0x4400000044000000ull;  // {512, 512}
-    using T = typename std::conditional<BF16, __nv_bfloat16, float>::type;
-    const uint32_t ow = OUT ? OUT : a.out_w;
-    const uint64_t plane = static_cast<uint64_t>(OUT ? OUT : a.out_h) * ow;
-    auto bilerp = [&](const uint4& r, uint32_t v[3]) {
-        uint32_t rg0, b0, rg1, b1;
-        row_taps_s(colword + r.x, sel, &rg0, &b0);
-        row_taps_s(colword + r.y, sel, &rg1, &b1);
-        const uint32_t w0 = colw * r.z, w1 = colw * r.w;  // two u16 lanes each, no carry
-        v[0] = __dp2a_lo(w0, rg0, __dp2a_lo(w1, rg1, kMagic14));
-        v[1] = __dp2a_hi(w0, rg0, __dp2a_hi(w1, rg1, kMagic14));
-        v[2] = __dp2a_lo(w0, b0, __dp2a_lo(w1, b1, kMagic14));
-    };
-    T* pc = static_cast<T*>(a.out) + k * 3 * plane + static_cast<uint64_t>(oy0) * ow + ox;
-    auto emit = [&](const uint32_t* v0, const uint32_t* v1, bool two) {
-#pragma unroll
-        for (uint32_t c = 0; c < 3; ++c) {
-            const uint64_t m = pk(v0[c], v1[c]);  // already 0x44000000 + v
-            const uint64_t o = mul2(sub2(sub2(m, k512), mean2[c]), inv2[c]);
-            T* pt = pc + c * plane;
-            if constexpr (BF16) {
-                const uint32_t h = bf16x2(o);
-                st_cs_u16(pt, static_cast<uint16_t>(h));
-                if (two) st_cs_u16(pt + ow, static_cast<uint16_t>(h >> 16));
-            } else {
-                st_cs_f32(pt, __uint_as_float(lo32(o)));
-                if (two) st_cs_f32(pt + ow, __uint_as_float(hi32(o)));
-            }
-        }
-        pc += 2 * ow;
-    };
-    uint32_t rr = 0;
-#pragma unroll 2
-    for (; rr + 1 < rows_out; rr += 2) {
-        uint32_t v0[3], v1[3];
-        bilerp(s_row[rr], v0);
-        bilerp(s_row[rr + 1], v1);
-        emit(v0, v1, true);
-    }
-    if (rr < rows_out) {  // odd band height
-        uint32_t v0[3];
-        bilerp(s_row[rr], v0);
-        emit(v0, v0, false);
-    }
-}
-
 __global__ void k_aug_params(uint64_t seed, uint64_t epoch, const uint64_t* __restrict__ ids,
                              uint64_t n, uint32_t H, uint32_t W, uint32_t out_h, uint32_t out_w,
                              int mode, uint32_t* __restrict__ out5) {
@@ -1029,35 +849,6 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
         // word-aligned rows: the variable-geometry shard layout (geometry.cuh)
         const bool aligned = src.prefix != nullptr;
         const bool out224 = spec.out_h == 224 && spec.out_w == 224;
-        // K7 staged (TMA rows into shared memory, LDS taps): variable-geometry
-        // shards (word-aligned rows), out_w <= 512; LL_K7=rows keeps the
-        // gather kernel for A/B runs
-        static const char* k7 = std::getenv("LL_K7");
-        const std::string k7v = k7 ? k7 : "staged8";
-        const uint32_t rb = k7v == "staged16" ? 16u : 8u;
-        const uint32_t cap = staged_rows_max(rb, kVarMin + kVarSpan - 1, spec.out_h);
-        const size_t smem = static_cast<size_t>(cap) * kStageStride;
-        if (aligned && k7v != "rows" && smem <= 200 * 1024) {
-            const dim3 sgrid(static_cast<unsigned>(n), (spec.out_h + rb - 1) / rb);
-            auto go = [&](auto kern) {
-                ensure_smem_attr(kern, ctx->device, smem);
-                kern<<<sgrid, threads, smem, ctx->stream>>>(a, it, cap);
-            };
-            launch(ctx, "augment_resize", [&] {
-                if (rb == 16) {
-                    if (bf16 && out224) go(k_augment_resize_staged<true, 16, 224>);
-                    else if (bf16) go(k_augment_resize_staged<true, 16>);
-                    else if (out224) go(k_augment_resize_staged<false, 16, 224>);
-                    else go(k_augment_resize_staged<false, 16>);
-                } else {
-                    if (bf16 && out224) go(k_augment_resize_staged<true, 8, 224>);
-                    else if (bf16) go(k_augment_resize_staged<true, 8>);
-                    else if (out224) go(k_augment_resize_staged<false, 8, 224>);
-                    else go(k_augment_resize_staged<false, 8>);
-                }
-            });
-            return;
-        }
         launch(ctx, "augment_resize", [&] {
             if (bf16 && aligned && out224)
                 k_augment_resize_rows<true, true, 224><<<grid, threads, 0, ctx->stream>>>(a, it);
