@@ -591,14 +591,8 @@ __device__ __forceinline__ void bilerp_a(const uint8_t* colp, uint32_t sel, uint
 // 64-bit add, three loads and four byte permutes.
 // OUT = 224 fixes the output geometry at compile time (cfg5), so all six
 // stores of a row pair address off one pointer with immediate offsets.
-// LL_K7_MAXNREG (variant builds for A/B): cap K7's registers
-#ifdef LL_K7_MAXNREG
-#define LL_K7_REGS __maxnreg__(LL_K7_MAXNREG)
-#else
-#define LL_K7_REGS __launch_bounds__(kMaxOutW)
-#endif
 template <bool BF16, bool ALIGNED, uint32_t OUT = 0>
-__global__ void LL_K7_REGS k_augment_resize_rows(AugArgs a,
+__global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
                                                                   const ResizeItem* items) {
     // {lo row offset, hi row offset, 128-wy, wy}; offsets from s_base, which is
     // the sample start (ALIGNED) or the sample start rounded down to 4 bytes
@@ -702,39 +696,12 @@ __global__ void LL_K7_REGS k_augment_resize_rows(AugArgs a,
         }
         if (OUT) pc[0] += 2 * ow;
     };
-    // A row pair taps each DISTINCT source row once: its two output rows
-    // often share one (1 < ch / out_h < 2: the first row's hi row is the
-    // second's lo row) or both (upsampling), and a row with wy = 0 has no hi
-    // row.  The row table is the same for the whole CTA, so these tests are
-    // uniform branches.
-    struct Taps {
-        uint32_t rg, b;
-    };
-    auto taps = [&](uint32_t rowoff) {
-        Taps t;
-        if constexpr (ALIGNED)
-            row_taps_a(colp + rowoff, sel, &t.rg, &t.b);
-        else
-            row_taps_g(base, rowoff + x3, &t.rg, &t.b);
-        return t;
-    };
-    auto combine = [&](const Taps& lo, const Taps& hi, const uint4& r, uint32_t v[3]) {
-        const uint32_t w0 = colw * r.z, w1 = colw * r.w;  // two u16 lanes each, no carry
-        v[0] = __dp2a_lo(w0, lo.rg, __dp2a_lo(w1, hi.rg, kMagic14));
-        v[1] = __dp2a_hi(w0, lo.rg, __dp2a_hi(w1, hi.rg, kMagic14));
-        v[2] = __dp2a_lo(w0, lo.b, __dp2a_lo(w1, hi.b, kMagic14));
-    };
     uint32_t rr = 0;
 #pragma unroll(OUT ? 2 : 1)
     for (; rr + 1 < rows_out; rr += 2) {
-        const uint4 ra = s_row[rr], rb = s_row[rr + 1];
-        const Taps a0 = taps(ra.x);
-        const Taps a1 = ra.w ? taps(ra.y) : a0;
-        const Taps b0 = rb.x == ra.x ? a0 : rb.x == ra.y ? a1 : taps(rb.x);
-        const Taps b1 = !rb.w ? b0 : rb.y == ra.y ? a1 : taps(rb.y);
         uint32_t v0[3], v1[3];
-        combine(a0, a1, ra, v0);
-        combine(b0, b1, rb, v1);
+        bilerp(s_row[rr], v0);
+        bilerp(s_row[rr + 1], v1);
         emit(v0, v1, true);
     }
     if (rr < rows_out) {  // odd band height
