@@ -210,10 +210,13 @@ __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint6
 
 // Rows [r_first, r_first + kBand) of the band: thread (tr, tq) writes pixel run
 // tq of rows tr, tr + PX, ...
+// phase (ROW16 = false): byte r of it is where source row r's data starts in
+// its smem row (the row was staged from the 16-byte-aligned address at or
+// below its window start); null when every row starts aligned.
 template <bool BF16>
 __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, uint32_t a0,
                                           uint64_t k, uint32_t band, const NormConst& nc,
-                                          void* out) {
+                                          void* out, const uint8_t* phase = nullptr) {
     constexpr uint32_t PX = BF16 ? 8 : 4;
     constexpr uint32_t TPR = kOut / PX;
     const uint32_t tr = threadIdx.x / TPR, tq = threadIdx.x - tr * TPR;
@@ -233,20 +236,26 @@ __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, 
     for (uint32_t rr = 0; rr < kBand / PX; ++rr) {
         const uint32_t r = rr * PX + tr;
         const uint64_t o = obase + static_cast<uint64_t>(r) * kOut;
+        const int32_t b = phase ? base + phase[r] : base;
         if (q.flip)
-            emit_run<BF16, true>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
+            emit_run<BF16, true>(rows + r * kRowSmem, b, mean2, inv2, out, o, plane);
         else
-            emit_run<BF16, false>(rows + r * kRowSmem, base, mean2, inv2, out, o, plane);
+            emit_run<BF16, false>(rows + r * kRowSmem, b, mean2, inv2, out, o, plane);
     }
 }
 
 // PX output pixels per thread: 4 (fp32, one float4 per plane) or 8 (bf16,
 // eight bf16 per plane).  kThreads/(224/PX) = PX rows per pass.
-template <bool BF16>
+// ROW16: source rows are a multiple of 16 bytes (256-px ImageNet shapes), so
+// every window row starts at the same 16-byte phase; otherwise (e.g. a
+// 250-px source, 750-byte rows) each row is staged from the aligned address
+// below its own window start and keeps its phase in s_phase.
+template <bool BF16, bool ROW16 = true>
 // (measured: 4 resident CTAs per SM at 72 registers beat forcing 5-9 by
 // register caps or a larger shared-memory carveout; profiles/r01_augment_ab.md)
 __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
+    __shared__ uint8_t s_phase[kBand];
     __shared__ const uint8_t* s_src;
     __shared__ Params s_prm;
     __shared__ uint64_t s_k;
@@ -296,9 +305,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     const bool win = s_win != 0;
     const uint32_t row_bytes = win ? kWinRow : a.W * 3;
     const uint32_t a0 = (3 * q.x0) & ~15u;
-    const uint32_t nch = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
+    const uint32_t nch0 = (((3 * q.x0 + 3 * kOut) + 15u) & ~15u) / 16 - a0 / 16;
     const uint8_t* gbase = win ? src + static_cast<uint64_t>(band * kBand) * kWinRow
                                : src + static_cast<uint64_t>(q.y0 + band * kBand) * row_bytes + a0;
+    // unaligned rows: row r is read from the aligned address below its
+    // window start, one more chunk when the phase pushes the span over
+    constexpr bool kAligned = ROW16;
+    const bool per_row = !kAligned && !win;
+    auto row_src = [&](uint32_t r) -> const uint8_t* {
+        const uint8_t* g = gbase + static_cast<uint64_t>(r) * row_bytes;
+        return per_row ? reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(g) &
+                                                          ~static_cast<uintptr_t>(15))
+                       : g;
+    };
+    const uint32_t nch = per_row ? nch0 + 1 : nch0;  // <= 44 chunks = kRowSmem
+    if (per_row && tid < kBand)
+        s_phase[tid] = static_cast<uint8_t>(
+            reinterpret_cast<uintptr_t>(gbase + static_cast<uint64_t>(tid) * row_bytes) & 15);
     if (s_host) {
         // far samples (host storage tier, peer shards): the band's 32 row
         // segments as TMA bulk copies instead of 16-byte loads (cfg3: 0.78 ->
@@ -312,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
                 const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&rows[r][0]));
                 asm volatile(
                     "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                    "l"(gbase + static_cast<uint64_t>(r) * row_bytes), "r"(nch * 16), "r"(mb)
+                    "l"(row_src(r)), "r"(nch * 16), "r"(mb)
                     : "memory");
             }
         }
@@ -332,8 +355,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
 #pragma unroll
         for (uint32_t i = 0; i < kIters; ++i) {
             const uint32_t t = tid + i * kThreads, r = t / kSlots, c = t - r * kSlots;
-            if (r < kBand && c < nch)
-                v[i] = ld_nc_v4(gbase + static_cast<uint64_t>(r) * row_bytes + 16 * c);
+            if (r < kBand && c < nch) v[i] = ld_nc_v4(row_src(r) + 16 * c);
         }
 #pragma unroll
         for (uint32_t i = 0; i < kIters; ++i) {
@@ -343,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
     }
     __syncthreads();
 
-    emit_band<BF16>(&rows[0][0], q, a0, k, band, a.nc, a.out);
+    emit_band<BF16>(&rows[0][0], q, a0, k, band, a.nc, a.out, per_row ? s_phase : nullptr);
 }
 
 // ---- K7: fixed-point bilinear resize (cfg5) ------------------------------
@@ -591,8 +613,13 @@ __device__ __forceinline__ void bilerp_a(const uint8_t* colp, uint32_t sel, uint
 // 64-bit add, three loads and four byte permutes.
 // OUT = 224 fixes the output geometry at compile time (cfg5), so all six
 // stores of a row pair address off one pointer with immediate offsets.
+#ifdef LL_K7_MAXNREG  // variant builds for A/B runs
+#define LL_K7_BOUNDS __maxnreg__(LL_K7_MAXNREG)
+#else
+#define LL_K7_BOUNDS __launch_bounds__(kMaxOutW)
+#endif
 template <bool BF16, bool ALIGNED, uint32_t OUT = 0>
-__global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
+__global__ void LL_K7_BOUNDS k_augment_resize_rows(AugArgs a,
                                                                   const ResizeItem* items) {
     // {lo row offset, hi row offset, 128-wy, wy}; offsets from s_base, which is
     // the sample start (ALIGNED) or the sample start rounded down to 4 bytes
@@ -697,6 +724,52 @@ __global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
         if (OUT) pc[0] += 2 * ow;
     };
     uint32_t rr = 0;
+#ifndef LL_K7_NOPIPE
+    if constexpr (ALIGNED && OUT != 0 && OUT % kRB == 0) {
+        // Software-pipelined: the twelve tap words of row pair i + 1 are in
+        // flight while pair i is combined, normalised and stored -- K7 is
+        // bound by tap-load latency, so words in flight per warp is the lever
+        // (profiles/r2_k7_ab.md).  Every band has kRB rows here.
+        auto load_pair = [&](uint32_t r, uint32_t* w) {
+            const uint4 ra = s_row[r], rb = s_row[r + 1];
+            const uint32_t offs[4] = {ra.x, ra.y, rb.x, rb.y};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const uint32_t* q = reinterpret_cast<const uint32_t*>(colp + offs[t]);
+                w[3 * t] = __ldg(q);
+                w[3 * t + 1] = __ldg(q + 1);
+                w[3 * t + 2] = __ldg(q + 2);
+            }
+        };
+        auto combine = [&](const uint32_t* w, int t0, const uint4& r, uint32_t v[3]) {
+            uint32_t rg[2], bb[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const uint32_t* x = w + 3 * (t0 + u);
+                const uint32_t ta = f4e(x[0], x[1], sel), tb = f4e(x[1], x[2], sel);
+                rg[u] = __byte_perm(ta, tb, 0x4130);
+                bb[u] = __byte_perm(ta, tb, 0x0052);
+            }
+            const uint32_t w0 = colw * r.z, w1 = colw * r.w;
+            v[0] = __dp2a_lo(w0, rg[0], __dp2a_lo(w1, rg[1], kMagic14));
+            v[1] = __dp2a_hi(w0, rg[0], __dp2a_hi(w1, rg[1], kMagic14));
+            v[2] = __dp2a_lo(w0, bb[0], __dp2a_lo(w1, bb[1], kMagic14));
+        };
+        uint32_t cur[12], nxt[12];
+        load_pair(0, cur);
+#pragma unroll
+        for (uint32_t i = 0; i < kRB / 2; ++i) {
+            if (i + 1 < kRB / 2) load_pair(2 * i + 2, nxt);
+            uint32_t v0[3], v1[3];
+            combine(cur, 0, s_row[2 * i], v0);
+            combine(cur, 2, s_row[2 * i + 1], v1);
+            emit(v0, v1, true);
+#pragma unroll
+            for (int t = 0; t < 12; ++t) cur[t] = nxt[t];
+        }
+        return;
+    }
+#endif
 #pragma unroll(OUT ? 2 : 1)
     for (; rr + 1 < rows_out; rr += 2) {
         uint32_t v0[3], v1[3];
@@ -741,7 +814,7 @@ static void validate_spec(const ll_augment_spec& spec, uint32_t H, uint32_t W) {
     if (spec.mode == LL_AUG_CROP) {
         require(spec.out_h == kOut && spec.out_w == kOut, "augment: crop output must be 224x224");
         require(H >= kOut && W >= kOut, "augment: source smaller than the crop");
-        require((3ull * W) % 16 == 0, "augment: source row bytes must be a multiple of 16");
+
     } else {
         require(spec.mode == LL_AUG_RESIZE, "augment: unknown mode");
         require(spec.out_h >= 1 && spec.out_w >= 1 && H >= 1 && W >= 1,
@@ -823,11 +896,19 @@ void augment_device(ll_ctx* ctx, const ll_augment_spec& spec, uint64_t seed, uin
     const bool bf16 = spec.out_dtype == LL_OUT_BF16;
     if (spec.mode == LL_AUG_CROP) {
         const dim3 grid(static_cast<unsigned>(n * kBands));
+        // sources whose rows (and samples) are 16-byte multiples keep one
+        // phase for every row; others (e.g. 250 px wide) stage per row
+        const bool row16 = (3ull * width) % 16 == 0 &&
+                           (src.kind != 0 || (reinterpret_cast<uintptr_t>(src.base) & 15) == 0);
         launch(ctx, "augment_crop", [&] {
-            if (bf16)
-                k_augment_crop<true><<<grid, kThreads, 0, ctx->stream>>>(a);
+            if (bf16 && row16)
+                k_augment_crop<true, true><<<grid, kThreads, 0, ctx->stream>>>(a);
+            else if (row16)
+                k_augment_crop<false, true><<<grid, kThreads, 0, ctx->stream>>>(a);
+            else if (bf16)
+                k_augment_crop<true, false><<<grid, kThreads, 0, ctx->stream>>>(a);
             else
-                k_augment_crop<false><<<grid, kThreads, 0, ctx->stream>>>(a);
+                k_augment_crop<false, false><<<grid, kThreads, 0, ctx->stream>>>(a);
         });
         return;
     }

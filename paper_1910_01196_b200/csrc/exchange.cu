@@ -35,11 +35,21 @@ __device__ __forceinline__ void copy_slot(const uint8_t* src, uint8_t* dst, uint
     const uint32_t a0 = (3 * x0) & ~15u;
     const uint32_t nch = ((3 * x0 + 3 * kWinRows + 15u) & ~15u) / 16 - a0 / 16;
     const uint8_t* s0 = src + static_cast<uint64_t>(y0) * row_bytes + a0;
-    for (uint32_t t = part * blockDim.x + threadIdx.x; t < kWinRows * nch;
-         t += parts * blockDim.x) {
-        const uint32_t r = t / nch, c = t - r * nch;
-        __stcs(reinterpret_cast<uint4*>(dst + r * kWinRow) + c,
-               __ldg(reinterpret_cast<const uint4*>(s0 + static_cast<uint64_t>(r) * row_bytes) + c));
+    if ((row_bytes & 15) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+        for (uint32_t t = part * blockDim.x + threadIdx.x; t < kWinRows * nch;
+             t += parts * blockDim.x) {
+            const uint32_t r = t / nch, c = t - r * nch;
+            __stcs(reinterpret_cast<uint4*>(dst + r * kWinRow) + c,
+                   __ldg(reinterpret_cast<const uint4*>(s0 + static_cast<uint64_t>(r) * row_bytes) + c));
+        }
+        return;
+    }
+    // unaligned rows (e.g. 250-px sources): the same bytes, realigned so the
+    // receiver reads every slot row from its start (K6's window-slot path)
+    const uint32_t nb = 16 * nch;
+    for (uint32_t t = part * blockDim.x + threadIdx.x; t < kWinRows * nb; t += parts * blockDim.x) {
+        const uint32_t r = t / nb, c = t - r * nb;
+        dst[r * kWinRow + c] = s0[static_cast<uint64_t>(r) * row_bytes + c];
     }
 }
 
@@ -178,7 +188,8 @@ void reg_prep_device(ll_ctx* ctx, const uint32_t* d_batch, const uint32_t* d_scr
                      const uint32_t* d_regcnt, uint32_t p, uint32_t me, uint64_t B,
                      const uint8_t* shard, uint64_t shard_first, uint64_t sample_bytes,
                      uint8_t* pack, uint32_t* ridx, const uint32_t* d_aug, uint32_t row_bytes) {
-    require(sample_bytes % 16 == 0, "exchange: sample bytes must be a multiple of 16");
+    require(d_aug != nullptr || sample_bytes % 16 == 0,
+            "exchange: whole-sample messages need sample bytes that are a multiple of 16");
     require(B % p == 0, "reg_slice: learner count must divide the batch size");
     RegPrepArgs a{d_batch, d_scratch, d_regcnt, p, me, static_cast<uint32_t>(B / p), shard,
                   shard_first, sample_bytes, pack, ridx, d_aug, row_bytes,
@@ -208,8 +219,8 @@ void pack_device(ll_ctx* ctx, const std::vector<ll_xfer>& xfers, const uint32_t*
         n_pack += x.count;
     }
     if (n_pack == 0) return;
-    require(rw.enabled || sample_bytes % 16 == 0,
-            "exchange: sample bytes must be a multiple of 16");
+    require(rw.enabled || d_aug != nullptr || sample_bytes % 16 == 0,
+            "exchange: whole-sample messages need sample bytes that are a multiple of 16");
     a.final_step = d_final_step;
     a.shard = shard;
     a.shard_first = shard_first;

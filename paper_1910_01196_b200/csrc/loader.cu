@@ -790,7 +790,9 @@ void populate_storage(ll_loader* ld) {
     const uint64_t n = ld->cfg.d - ld->cached;
     if (n == 0 || ld->storage) return;
     ll_ctx* ctx = ld->ctx;
-    LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ld->storage), n * ld->S,
+    // + 64: window rows are read from the 16-byte-aligned address at or below
+    // them and may run up to 31 bytes past the last sample (K6, unaligned rows)
+    LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ld->storage), n * ld->S + 64,
                           cudaHostAllocMapped | cudaHostAllocPortable));
     const uint64_t chunk = std::max<uint64_t>(1, (1ull << 30) / ld->S);
     DevBuf& tmp = ctx->buf("storage.stage", chunk * ld->S);
@@ -988,7 +990,7 @@ void loader_populate_from_files(ll_loader* ld, const char* root_c, uint32_t thre
     const uint64_t n_unc = c.d - ld->cached;
     if (n_unc) {
         if (!ld->storage)
-            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ld->storage), n_unc * ld->S,
+            LL_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ld->storage), n_unc * ld->S + 64,
                                   cudaHostAllocMapped | cudaHostAllocPortable));
         read_files(ld, root, ld->cached, c.d, ld->storage,
                    [&](uint64_t s) { return (s - ld->cached) * ld->S; }, threads);

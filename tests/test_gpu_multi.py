@@ -180,7 +180,7 @@ def test_two_learners_variable_resize(tmp_path, exchange):
 
 
 @pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("hw", [(224, 224), (232, 224)])
+@pytest.mark.parametrize("hw", [(224, 224), (232, 224), (250, 250)])
 def test_two_learners_nccl_small_sources(tmp_path, hw):
     """Sources whose whole sample is smaller than a crop-window message slot
     (224 x 224, 232 x 224): the exchange buffers are sized by the slot at

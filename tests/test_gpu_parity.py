@@ -304,6 +304,57 @@ def test_crop_augment_non_square_source():
         assert np.array_equal(got[k], oracle.augment(src[k].reshape(H, W, 3), k, 5, 0))
 
 
+@pytest.mark.parametrize("hw", [(250, 250), (230, 229), (224, 225), (301, 226)])
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_crop_augment_unaligned_rows(hw, dtype):
+    """Sources whose rows are not a multiple of 16 bytes (750, 687, 675, 678
+    bytes): K6 stages every row from the aligned address below its own window
+    start; bit-exact vs the oracle (the 256-px layout keeps one phase)."""
+    H, W = hw
+    ids = np.arange(11, dtype=np.uint64) * 7 + 3
+    src = oracle.gen_samples(9, ids, H * W * 3)
+    got = device_augment(src, ids, H, W, 13, 2, dtype=dtype)
+    for k, sid in enumerate(ids):
+        want = oracle.augment(src[k].reshape(H, W, 3), int(sid), 13, 2, bf16=dtype == "bf16")
+        assert np.array_equal(got[k], want), (hw, k)
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("alpha", [1.0, 0.5])
+def test_loader_unaligned_rows_p2p_and_storage(dtype, alpha):
+    """250 x 250 sources through the loader: own shard, a peer shard over the
+    P2P path (TMA row copies from the aligned address) and, with alpha = 0.5,
+    the host storage tier."""
+    d, p, B, seed, H = 2000, 2, 96, 42, 250
+    lds = []
+    for j in range(p):
+        ld = DeviceLoader(LoaderConfig(d=d, height=H, width=H, learners=p, rank=j, batch_size=B,
+                                       alpha=alpha, seed=seed, data_seed=seed, exchange="p2p",
+                                       augment=AugmentConfig(out_dtype=dtype)))
+        ld.populate()
+        lds.append(ld)
+    DeviceLoader.link_peers(lds)
+    order = oracle.permute_epoch(seed, 1, d)
+    cached = oracle.cached_count(d, alpha)
+    far = 0
+    for t in [0, 5]:
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, cached, oracle.MODE_LOCALITY_BALANCED)
+        for j, ld in enumerate(lds):
+            info = ld.step(1, t)
+            lst = r["final_ids"][r["final_off"][j]:r["final_off"][j + 1]]
+            assert np.array_equal(ld.fetch_ids(info), lst)
+            got = ld.fetch(info)
+            src = oracle.gen_samples(seed, lst, H * H * 3)
+            for k, sid in enumerate(lst):
+                want = oracle.augment(src[k].reshape(H, H, 3), int(sid), seed, 1,
+                                      bf16=dtype == "bf16")
+                assert np.array_equal(got[k], want), (t, j, k)
+            far += len(lst) - info.kept
+    assert far > 0
+    for ld in lds:
+        ld.close()
+
+
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 def test_resize_augment_vs_oracle(dtype):
     for sid in [1, 2, 3, 4]:
