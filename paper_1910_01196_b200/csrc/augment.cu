@@ -613,13 +613,8 @@ __device__ __forceinline__ void bilerp_a(const uint8_t* colp, uint32_t sel, uint
 // 64-bit add, three loads and four byte permutes.
 // OUT = 224 fixes the output geometry at compile time (cfg5), so all six
 // stores of a row pair address off one pointer with immediate offsets.
-#ifdef LL_K7_MAXNREG  // variant builds for A/B runs
-#define LL_K7_BOUNDS __maxnreg__(LL_K7_MAXNREG)
-#else
-#define LL_K7_BOUNDS __launch_bounds__(kMaxOutW)
-#endif
 template <bool BF16, bool ALIGNED, uint32_t OUT = 0>
-__global__ void LL_K7_BOUNDS k_augment_resize_rows(AugArgs a,
+__global__ void __launch_bounds__(kMaxOutW) k_augment_resize_rows(AugArgs a,
                                                                   const ResizeItem* items) {
     // {lo row offset, hi row offset, 128-wy, wy}; offsets from s_base, which is
     // the sample start (ALIGNED) or the sample start rounded down to 4 bytes
@@ -724,52 +719,6 @@ __global__ void LL_K7_BOUNDS k_augment_resize_rows(AugArgs a,
         if (OUT) pc[0] += 2 * ow;
     };
     uint32_t rr = 0;
-#ifndef LL_K7_NOPIPE
-    if constexpr (ALIGNED && OUT != 0 && OUT % kRB == 0) {
-        // Software-pipelined: the twelve tap words of row pair i + 1 are in
-        // flight while pair i is combined, normalised and stored -- K7 is
-        // bound by tap-load latency, so words in flight per warp is the lever
-        // (profiles/r2_k7_ab.md).  Every band has kRB rows here.
-        auto load_pair = [&](uint32_t r, uint32_t* w) {
-            const uint4 ra = s_row[r], rb = s_row[r + 1];
-            const uint32_t offs[4] = {ra.x, ra.y, rb.x, rb.y};
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                const uint32_t* q = reinterpret_cast<const uint32_t*>(colp + offs[t]);
-                w[3 * t] = __ldg(q);
-                w[3 * t + 1] = __ldg(q + 1);
-                w[3 * t + 2] = __ldg(q + 2);
-            }
-        };
-        auto combine = [&](const uint32_t* w, int t0, const uint4& r, uint32_t v[3]) {
-            uint32_t rg[2], bb[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const uint32_t* x = w + 3 * (t0 + u);
-                const uint32_t ta = f4e(x[0], x[1], sel), tb = f4e(x[1], x[2], sel);
-                rg[u] = __byte_perm(ta, tb, 0x4130);
-                bb[u] = __byte_perm(ta, tb, 0x0052);
-            }
-            const uint32_t w0 = colw * r.z, w1 = colw * r.w;
-            v[0] = __dp2a_lo(w0, rg[0], __dp2a_lo(w1, rg[1], kMagic14));
-            v[1] = __dp2a_hi(w0, rg[0], __dp2a_hi(w1, rg[1], kMagic14));
-            v[2] = __dp2a_lo(w0, bb[0], __dp2a_lo(w1, bb[1], kMagic14));
-        };
-        uint32_t cur[12], nxt[12];
-        load_pair(0, cur);
-#pragma unroll
-        for (uint32_t i = 0; i < kRB / 2; ++i) {
-            if (i + 1 < kRB / 2) load_pair(2 * i + 2, nxt);
-            uint32_t v0[3], v1[3];
-            combine(cur, 0, s_row[2 * i], v0);
-            combine(cur, 2, s_row[2 * i + 1], v1);
-            emit(v0, v1, true);
-#pragma unroll
-            for (int t = 0; t < 12; ++t) cur[t] = nxt[t];
-        }
-        return;
-    }
-#endif
 #pragma unroll(OUT ? 2 : 1)
     for (; rr + 1 < rows_out; rr += 2) {
         uint32_t v0[3], v1[3];
