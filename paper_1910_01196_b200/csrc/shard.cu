@@ -28,8 +28,9 @@ __device__ __forceinline__ void gen_chunk(uint8_t* dst_sample, uint64_t key, uin
         st_cs_v4(dst_sample + byte0,
                  make_uint4(static_cast<uint32_t>(w0), static_cast<uint32_t>(w0 >> 32),
                             static_cast<uint32_t>(w1), static_cast<uint32_t>(w1 >> 32)));
-    } else {
-        for (uint64_t b = byte0; b < sample_bytes; ++b) {
+    } else {  // unaligned sample sizes, or the sample's tail chunk
+        const uint64_t end = byte0 + 16 < sample_bytes ? byte0 + 16 : sample_bytes;
+        for (uint64_t b = byte0; b < end; ++b) {
             const uint64_t w = (b - byte0) < 8 ? w0 : w1;
             dst_sample[b] = static_cast<uint8_t>(w >> (((b - byte0) & 7) * 8));
         }

@@ -266,6 +266,20 @@ def test_generated_bytes_match_reference_golden(golden):
         assert hashlib.sha256(out.tobytes()).hexdigest() == c["sha256"]
 
 
+@pytest.mark.parametrize("nbytes", [187500, 1000, 17, 150528 + 8])
+def test_generated_bytes_unaligned_sizes_vs_oracle(nbytes):
+    """K1 with sample sizes that are not multiples of 16 (250 x 250 x 3 =
+    187,500 B, ...): every 16-byte chunk writes exactly its own bytes."""
+    import ctypes as C
+    ids = np.array([0, 5, 77, 123456], np.uint64)
+    out = np.empty(len(ids) * nbytes, np.uint8)
+    _capi.check(_capi.lib().ll_generate_samples(ll.locload.context(), 42,
+                                                _capi.ptr(ids, C.c_uint64), len(ids), nbytes,
+                                                _capi.ptr(out, C.c_uint8)))
+    want = oracle.gen_samples(42, ids, nbytes)
+    assert np.array_equal(out.reshape(len(ids), nbytes), want)
+
+
 # ------------------------------------------------------------- augment (K6/K7)
 def device_augment(src, ids, H, W, seed, epoch, mode="crop", dtype="fp32", oh=224, ow=224):
     import ctypes as C
