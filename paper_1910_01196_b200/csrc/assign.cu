@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
                 imb[j] = static_cast<long long>(cnt[j]) -
                          static_cast<long long>(base + (j < rem ? 1u : 0u));
             nmv = greedy_balance(imb, p, mv);
+            LL_DCHECK(nmv + 1 <= p || nmv == 0);
             uint32_t taken[kMaxP], recvd[kMaxP];
             for (uint32_t j = 0; j < p; ++j) taken[j] = recvd[j] = 0;
             for (uint32_t m = 0; m < nmv; ++m) {
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(kThreads) k_assign(AssignArgs a, PlanDev P) {
                 }
             }
         }
+        LL_DCHECK(fj < p && off[fj] + fk < off[fj + 1] && off[fj + 1] <= B);
         final_ids[off[fj] + fk] = s;
         if (a.aug.enabled) P.aug[st * B + off[fj] + fk] = crop_params(a.aug, s);
     }

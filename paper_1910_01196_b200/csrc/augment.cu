@@ -104,9 +104,13 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
         // storage tier (alpha < 1): uncached samples from mapped pinned host memory
         *src = m.storage + (s - m.cached) * m.sample_bytes;
         if (far) *far = true;
+        LL_DCHECK(!m.storage_end || *src + m.sample_bytes <= m.storage_end);
     } else if (k < kept) {
+        LL_DCHECK(s >= m.shard_first && s < m.cached);
         *src = m.shard + (m.prefix ? m.prefix[s] - m.prefix[m.shard_first]
                                    : (s - m.shard_first) * m.sample_bytes);
+        LL_DCHECK(!m.shard_end || m.prefix || *src + m.sample_bytes <= m.shard_end);
+        LL_DCHECK(!m.shard_end || !m.prefix || *src + (m.prefix[s + 1] - m.prefix[s]) <= m.shard_end);
     } else if (m.peers) {
         const uint32_t o = static_cast<uint32_t>(s * m.p / m.cached);
         const uint64_t first = (static_cast<uint64_t>(o) * m.cached + m.p - 1) / m.p;
@@ -170,6 +174,7 @@ __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint6
     constexpr int PX = BF16 ? 8 : 4;
     constexpr int NB = 3 * PX;      // 12 or 24 source bytes
     constexpr int NW = NB / 4 + 1;  // words covering them at any alignment
+    LL_DCHECK(base >= 0 && base + NB <= static_cast<int32_t>(kRowSmem));
     const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (base >> 2);
     const uint32_t sh = 8u * static_cast<uint32_t>(base & 3);
     uint32_t raw[NW];
@@ -319,6 +324,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_augment_crop(AugArgs a) {
                        : g;
     };
     const uint32_t nch = per_row ? nch0 + 1 : nch0;  // <= 44 chunks = kRowSmem
+    LL_DCHECK(nch * 16 <= kRowSmem);
+    LL_DCHECK(win || (q.y0 + kOut <= a.H && q.x0 + kOut <= a.W));
     if (per_row && tid < kBand)
         s_phase[tid] = static_cast<uint8_t>(
             reinterpret_cast<uintptr_t>(gbase + static_cast<uint64_t>(tid) * row_bytes) & 15);
@@ -483,6 +490,7 @@ __global__ void k_resize_prep(AugArgs a, ResizeItem* __restrict__ items, uint64_
     if (a.src.prefix) var_hw(a.src.data_seed, id, &H, &W);
     it.pitch = a.src.prefix ? var_pitch(W) : 3 * W;
     it.q = aug_params(a.seed, a.epoch, id, H, W, a.out_h, a.out_w, LL_AUG_RESIZE);
+    LL_DCHECK(it.q.y0 + it.q.ch <= H && it.q.x0 + it.q.cw <= W && 3 * W <= it.pitch);
     // a received resize window (NCCL): row y0 sits at byte kRecvPad of the slot
     if (win) it.src = it.src + kRecvPad - static_cast<uint64_t>(it.q.y0) * it.pitch;
     it.from = nullptr;

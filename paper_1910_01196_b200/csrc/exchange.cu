@@ -115,6 +115,7 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs a) {
     while (m + 1 < a.n_sends && rem >= a.count[m]) rem -= a.count[m++];
     const uint32_t fi = a.list_first[m] + static_cast<uint32_t>(rem);
     const uint32_t id = a.final_step[fi];
+    LL_DCHECK(m < a.n_sends && rem < a.count[m] && id >= a.shard_first);
     if (a.rw.enabled) {
         const uint8_t* sample;
         uint32_t pitch, y0, ch;

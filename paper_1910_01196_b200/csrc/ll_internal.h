@@ -30,6 +30,25 @@ inline void cuda_check(cudaError_t e, const char* what) {
 }
 #define LL_CUDA(x) ::ll::cuda_check((x), #x)
 
+// Device-side bounds / invariant checks, compiled in only for the checked
+// variant library (-DLL_CHECKED, scripts/checked_build.py): compute-sanitizer
+// is closed on this GPU pool, so the test suite runs against that build
+// instead (profiles/r2_sanitize/).  A failed check prints and traps.
+#ifdef LL_CHECKED
+#define LL_DCHECK(c)                                                                     \
+    do {                                                                                 \
+        if (!(c)) {                                                                      \
+            printf("LL_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+                   #c, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x));      \
+            __trap();                                                                    \
+        }                                                                                \
+    } while (0)
+#else
+#define LL_DCHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 // Device buffer with grow-only reallocation.
 struct DevBuf {
     void* ptr = nullptr;
@@ -207,6 +226,8 @@ struct SrcMap {
     const uint32_t* kept_dev = nullptr;  // if set: kept = *kept_dev (device)
     const uint32_t* aug = nullptr;       // plan-precomputed crop params, list-aligned
     const uint8_t* shard = nullptr;
+    const uint8_t* shard_end = nullptr;    // checked builds: the shard's last byte + 1
+    const uint8_t* storage_end = nullptr;  // ... and the storage tier's
     uint64_t shard_first = 0;
     const uint8_t* recv = nullptr;     // NCCL path: received samples in list order
     const uint8_t* const* peers = nullptr;  // P2P path: every learner's shard

@@ -89,6 +89,10 @@ struct ll_loader {
     // augment runs (two buffer sets, alternating by step parity)
     ExSet xset[2];
     cudaEvent_t xdone[2] = {nullptr, nullptr}, augdone[2] = {nullptr, nullptr};
+    // the pack kernel of a set runs on its own stream, so step t+1's pack
+    // overlaps step t's grouped send/recv on the side stream
+    cudaStream_t pack_stream = nullptr;
+    cudaEvent_t packdone[2] = {nullptr, nullptr};
     struct Pending {
         bool valid = false;
         uint64_t epoch = 0, step = 0;
@@ -134,7 +138,7 @@ struct ll_loader {
     // NCCL exchange accounting: bytes every step; with the context's timing
     // on, events around each step's pack and wire phase on its stream
     struct XTimes {
-        cudaEvent_t t0, t1, t2;
+        cudaEvent_t t0, t1, t2, t3;  // pack start / end (pack stream), wire start / end
         uint64_t recvd;
     };
     std::vector<XTimes> xtimes;
@@ -234,35 +238,41 @@ void ensure_out(ll_loader* ld) {
 //  * regular scheme (reg_slice, sampling.cpp:27-42): every learner exchanges
 //    with every other its owned samples of their slices (h_regcnt: this
 //    step's [slice][owner] counts); x.ridx maps slice positions to x.recv.
-// Brackets one step's exchange on its stream: pack kernel (t0 -> t1) and
-// NCCL grouped send/recv (t1 -> t2), while the context's timing is on.
+// Brackets one step's exchange: the pack kernel on the pack stream (t0 -> t1)
+// and the NCCL grouped send/recv on the wire stream (t2 -> t3, from the point
+// the wire stream has the packed set), while the context's timing is on.
 struct ExchangeTimer {
     ll_loader* ld;
-    cudaStream_t stream;
-    ll_loader::XTimes t{nullptr, nullptr, nullptr, 0};
-    ExchangeTimer(ll_loader* l, cudaStream_t s) : ld(l), stream(s) {
+    cudaStream_t pstream, wstream;
+    ll_loader::XTimes t{nullptr, nullptr, nullptr, nullptr, 0};
+    ExchangeTimer(ll_loader* l, cudaStream_t ps, cudaStream_t ws) : ld(l), pstream(ps), wstream(ws) {
         if (!ld->ctx->timing) return;
         t.t0 = ld->ctx->take_event();
-        LL_CUDA(cudaEventRecord(t.t0, stream));
+        LL_CUDA(cudaEventRecord(t.t0, pstream));
     }
     void packed() {
         if (!t.t0) return;
         t.t1 = ld->ctx->take_event();
-        LL_CUDA(cudaEventRecord(t.t1, stream));
+        LL_CUDA(cudaEventRecord(t.t1, pstream));
+    }
+    void wire_start() {
+        if (!t.t0) return;
+        t.t2 = ld->ctx->take_event();
+        LL_CUDA(cudaEventRecord(t.t2, wstream));
     }
     void done(uint64_t sent, uint64_t recvd) {
         ++ld->x_steps;
         ld->x_sent += sent;
         ld->x_recv += recvd;
         if (!t.t0) return;
-        t.t2 = ld->ctx->take_event();
-        LL_CUDA(cudaEventRecord(t.t2, stream));
+        t.t3 = ld->ctx->take_event();
+        LL_CUDA(cudaEventRecord(t.t3, wstream));
         t.recvd = recvd;
         ld->xtimes.push_back(t);
-        t = ll_loader::XTimes{nullptr, nullptr, nullptr, 0};  // owned by xtimes now
+        t = ll_loader::XTimes{nullptr, nullptr, nullptr, nullptr, 0};  // owned by xtimes now
     }
     ~ExchangeTimer() {  // an exception before done(): hand the events back
-        for (cudaEvent_t e : {t.t0, t.t1, t.t2})
+        for (cudaEvent_t e : {t.t0, t.t1, t.t2, t.t3})
             if (e) ld->ctx->event_pool.push_back(e);
     }
 };
@@ -275,9 +285,30 @@ uint64_t msg_slot(const ll_loader* ld) {
     return resize_slot_bytes(c.geometry == LL_GEOM_VARIABLE, c.height, c.width);
 }
 
+void ensure_pack_stream(ll_loader* ld) {
+    if (ld->pack_stream) return;
+    int lo = 0, hi = 0;
+    LL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    LL_CUDA(cudaStreamCreateWithPriority(&ld->pack_stream, cudaStreamNonBlocking, hi));
+    for (int i = 0; i < 2; ++i)
+        LL_CUDA(cudaEventCreateWithFlags(&ld->packdone[i], cudaEventDisableTiming));
+}
+
+// Exchange set `set` (xset[set]) for one step: the pack kernel on the pack
+// stream once the set is free again (its previous grouped send/recv,
+// xdone[set], and the augment that read it, augdone[set], are done), then the
+// grouped send/recv on `stream` after the pack.  So the pack of step t+1
+// overlaps the send/recv of step t.
 void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t step,
                     const ll_move* h_moves, uint32_t h_nmoves, const uint32_t* h_off,
-                    const uint32_t* h_regcnt, ll_loader::ExSet& x, cudaStream_t stream) {
+                    const uint32_t* h_regcnt, int set, cudaStream_t stream,
+                    cudaEvent_t plan_ready = nullptr) {
+    ll_loader::ExSet& x = ld->xset[set];
+    ensure_pack_stream(ld);
+    cudaStream_t ps = ld->pack_stream;
+    if (plan_ready) LL_CUDA(cudaStreamWaitEvent(ps, plan_ready, 0));  // host-driven step's plan
+    if (ld->xdone[set]) LL_CUDA(cudaStreamWaitEvent(ps, ld->xdone[set], 0));
+    if (ld->augdone[set]) LL_CUDA(cudaStreamWaitEvent(ps, ld->augdone[set], 0));
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
@@ -291,7 +322,14 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t s
     const uint64_t slot = msg_slot(ld);
     const uint32_t* d_aug = crop ? pd.aug + step * B : nullptr;
     const uint32_t row_bytes = 3 * c.width;
-    ExchangeTimer tm(ld, stream);
+    ExchangeTimer tm(ld, ps, stream);
+    // after the pack: the wire stream picks the set up
+    auto handoff = [&] {
+        tm.packed();
+        LL_CUDA(cudaEventRecord(ld->packdone[set], ps));
+        LL_CUDA(cudaStreamWaitEvent(stream, ld->packdone[set], 0));
+        tm.wire_start();
+    };
     if (c.scheme == LL_SCHEME_REGULAR) {
         require(crop, "loader: the regular scheme over NCCL needs crop mode (resize windows of "
                       "a full slice exchange go over the P2P exchange)");
@@ -300,7 +338,7 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t s
         x.pack.need(B * slot, "exchange send buffer");
         x.recv.need(B * slot, "exchange receive buffer");
         x.ridx.need(sizeof(uint32_t) * std::max<uint64_t>(L, 1), "exchange receive map");
-        ctx->stream = stream;
+        ctx->stream = ps;
         try {
             reg_prep_device(ctx, d_final_step, pd.scratch + step * B, pd.regcnt + step * p * p, p,
                             me, B, ld->shard.as<uint8_t>(), ld->first, ld->S,
@@ -310,7 +348,7 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t s
             throw;
         }
         ctx->stream = main;
-        tm.packed();
+        handoff();
         uint64_t sent = 0, recvd = 0;
         LL_NCCL(ncclGroupStart());
         for (uint32_t r = 0; r < p; ++r) {
@@ -365,7 +403,7 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t s
         rw.out_w = c.augment.out_w;
         rw.slot = slot;
     }
-    ctx->stream = stream;  // pack_device launches on the context stream
+    ctx->stream = ps;  // pack_device launches on the context stream
     try {
         pack_device(ctx, xs, d_final_step, ld->shard.as<uint8_t>(), ld->first, ld->S,
                     x.pack.as<uint8_t>(), d_aug, row_bytes, rw);
@@ -374,7 +412,7 @@ void issue_exchange(ll_loader* ld, const PlanDev& pd, uint64_t epoch, uint64_t s
         throw;
     }
     ctx->stream = main;
-    tm.packed();
+    handoff();
     uint64_t sent = 0, recvd = 0;
     LL_NCCL(ncclGroupStart());
     for (const ll_xfer& xf : xs) {
@@ -421,6 +459,8 @@ StepSrc step_src(ll_loader* ld, const PlanDev& pd, uint64_t step, const ll_move*
     src.list = d_final_step + h_off[me];
     src.kept = static_cast<uint32_t>(kept);
     src.shard = ld->shard.as<uint8_t>();
+    src.shard_end = ld->shard.as<uint8_t>() + ld->shard.bytes;
+    src.storage_end = ld->storage ? ld->storage + (ld->cfg.d - ld->cached) * ld->S + 64 : nullptr;
     src.shard_first = ld->first;
     src.p = p;
     src.cached = ld->cached;
@@ -526,6 +566,8 @@ SrcMap devplan_src(ll_loader* ld, const PlanDev& pd) {
     src.list_off = pd.off + me;
     src.kept_dev = pd.kept + me;
     src.shard = ld->shard.as<uint8_t>();
+    src.shard_end = ld->shard.as<uint8_t>() + ld->shard.bytes;
+    src.storage_end = ld->storage ? ld->storage + (ld->cfg.d - ld->cached) * ld->S + 64 : nullptr;
     src.shard_first = ld->first;
     src.p = p;
     src.cached = ld->cached;
@@ -683,7 +725,9 @@ void loader_destroy(ll_loader* ld) {
         if (h.done) cudaEventDestroy(h.done);
     }
     if (ld->side) cudaStreamDestroy(ld->side);
+    if (ld->pack_stream) cudaStreamDestroy(ld->pack_stream);
     for (int i = 0; i < 2; ++i) {
+        if (ld->packdone[i]) cudaEventDestroy(ld->packdone[i]);
         if (ld->xdone[i]) cudaEventDestroy(ld->xdone[i]);
         if (ld->rready[i]) cudaEventDestroy(ld->rready[i]);
         if (ld->rdone[i]) cudaEventDestroy(ld->rdone[i]);
@@ -1120,7 +1164,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             (void)kept;
             (void)st;
             issue_exchange(ld, ld->plan().view(), epoch, step, mv, nm, off, regcnt(step),
-                           ld->xset[slot], ld->side);
+                           static_cast<int>(slot), ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[slot], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
         }
@@ -1196,7 +1240,7 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             (void)kept;
             (void)st;
             issue_exchange(ld, ld->plan().view(), epoch, step + 1, mv, nm, off, regcnt(step + 1),
-                           ld->xset[ns], ld->side);
+                           static_cast<int>(ns), ld->side);
             LL_CUDA(cudaEventRecord(ld->xdone[ns], ld->side));
             ld->xpending[ns] = {true, epoch, step + 1};
         }
@@ -1339,7 +1383,7 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[xs], 0));
             // a loader_step prefetch parked in this set is clobbered now
             ld->xpending[xs].valid = false;
-            issue_exchange(ld, pd, epoch, 0, t->moves, t->n, t->off, rc, ld->xset[xs], ld->side);
+            issue_exchange(ld, pd, epoch, 0, t->moves, t->n, t->off, rc, xs, ld->side, h.pro_done);
             LL_CUDA(cudaEventRecord(ld->xdone[xs], ld->side));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[xs], 0));
             pre = &ld->xset[xs];
@@ -1428,15 +1472,15 @@ void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_
 void loader_exchange_stats(ll_loader* ld, double* out8, int reset) {
     set_device(ld->ctx);
     for (const auto& t : ld->xtimes) {
-        LL_CUDA(cudaEventSynchronize(t.t2));
         float a = 0, b = 0;
+        LL_CUDA(cudaEventSynchronize(t.t3));
         LL_CUDA(cudaEventElapsedTime(&a, t.t0, t.t1));
-        LL_CUDA(cudaEventElapsedTime(&b, t.t1, t.t2));
+        LL_CUDA(cudaEventElapsedTime(&b, t.t2, t.t3));
         ld->x_ms_pack += a;
         ld->x_ms_wire += b;
         ++ld->x_timed;
         ld->x_timed_recv += t.recvd;
-        for (cudaEvent_t e : {t.t0, t.t1, t.t2}) ld->ctx->event_pool.push_back(e);
+        for (cudaEvent_t e : {t.t0, t.t1, t.t2, t.t3}) ld->ctx->event_pool.push_back(e);
     }
     ld->xtimes.clear();
     out8[0] = static_cast<double>(ld->x_steps);

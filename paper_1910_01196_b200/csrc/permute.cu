@@ -121,6 +121,7 @@ __device__ __forceinline__ uint32_t run_round(const PermArgs& a, const uint2* cu
 #pragma unroll
         for (uint32_t u = 0; u < kU; ++u) {
             if (j[u] == i[u]) continue;  // padding or a no-op swap
+            LL_DCHECK(i[u] < a.d && j[u] < a.d && j[u] > i[u]);
             const unsigned long long key = prio(round, i[u]);
             atomicMax(a.R + i[u], key);
             atomicMax(a.R + j[u], key);
@@ -209,9 +210,11 @@ __device__ uint32_t smem_tail(const PermArgs& a, const uint2* cur, uint32_t n, u
     for (uint32_t h = tid; h < kTab; h += blockDim.x) keys[h] = kEmpty;
     if (tid < 2) cnt[tid] = 0;
     __syncthreads();
+    LL_DCHECK(n <= kTail);
     for (uint32_t t = tid; t < n; t += blockDim.x) {
         const uint2 v = __ldcg(cur + t);
         const uint32_t i = v.x, j = v.y;
+        LL_DCHECK(i < a.d && j < a.d);
         sidx[t] = i;
         si[t] = tab_slot(keys, aval, a.A, i);
         sj[t] = tab_slot(keys, aval, a.A, j);

@@ -14,11 +14,13 @@ run() {
   echo "bench $name rc=$?"; tail -1 gpurun_out/bench_${TAG}_n${N}_${name}.log | python -c "
 import json,sys
 try:
-    l=json.loads(sys.stdin.read()); print(round(l['value']), round(l['ms_per_step'],4), 'e2e', round(l['e2e']['value']) if l.get('e2e') else None, 'roof', round(l['roofline']['frac'],3), l['remote_per_epoch'])
+    l=json.loads(sys.stdin.read()); x=l.get('exchange') or {}; print(round(l['value']), round(l['ms_per_step'],4), 'e2e', round(l['e2e']['value']) if l.get('e2e') else None, 'roof', round(l['roofline']['frac'],3), 'nvlink', x.get('nvlink_gbs'))
 except Exception as e: print('parse fail', e)"
 }
 run cfg2_p2p --steps ${STEPS:-624}
 run cfg2_nccl --steps ${STEPS:-624} --exchange nccl
 run cfg3 --workload cfg3 --steps ${STEPS:-312}
 run cfg4 --workload cfg4 --steps ${STEPS:-312}
+run cfg4_nccl --workload cfg4 --exchange nccl --steps ${STEPS:-312}
 run cfg5 --workload cfg5 --steps ${STEPS:-312}
+run cfg5_nccl --workload cfg5 --exchange nccl --steps ${STEPS:-312}

@@ -1,0 +1,15 @@
+# r2m (2 GPUs): the GPU suite against the checked build (device bounds checks;
+# compute-sanitizer is closed on this pool), the multi-GPU suite on the
+# default build (NCCL pack on its own stream), cfg4 / cfg2 over NCCL at N = 2.
+mkdir -p gpurun_out/checked
+LL_LIB=variants/liblocload_checked.so timeout 1500 python -m pytest tests -m gpu -q -rf > gpurun_out/checked/pytest_checked.log 2>&1; echo "checked rc=$?" >> gpurun_out/checked/pytest_checked.log
+timeout 900 python -m pytest tests/test_gpu_multi.py -x -q > gpurun_out/r2m_multi.log 2>&1; echo rc=$? >> gpurun_out/r2m_multi.log
+for w in cfg4 cfg2; do
+  timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29531 bench.py --gpus 2 --workload $w --exchange nccl --steps 624 --warmup 20 > /tmp/o.json 2>> gpurun_out/r2m_bench.err
+  grep '^{' /tmp/o.json >> gpurun_out/r2m_bench.jsonl
+  python -c "
+import json; d=[json.loads(l) for l in open('/tmp/o.json') if l.startswith('{')][0]; x=d['exchange']
+print('$w', round(d['value']/1e6,3), round(d['ms_per_step'],4), round(x['wire_ms_per_step'],4), round(x['pack_ms_per_step'],4), round(x['nvlink_gbs'],1), round(x['frac'],3), d['e2e'] and round(d['e2e']['value']/1e6,3))
+" >> gpurun_out/r2m_ab.txt
+done
+tail -3 gpurun_out/checked/pytest_checked.log; tail -2 gpurun_out/r2m_multi.log; cat gpurun_out/r2m_ab.txt
