@@ -93,6 +93,9 @@ struct ll_loader {
     // overlaps step t's grouped send/recv on the side stream
     cudaStream_t pack_stream = nullptr;
     cudaEvent_t packdone[2] = {nullptr, nullptr};
+    // the grouped send/recv of every step, on a stream of its own so a
+    // host-driven step's prologue (side stream) never queues behind them
+    cudaStream_t wire_stream = nullptr;
     struct Pending {
         bool valid = false;
         uint64_t epoch = 0, step = 0;
@@ -292,6 +295,15 @@ void ensure_pack_stream(ll_loader* ld) {
     LL_CUDA(cudaStreamCreateWithPriority(&ld->pack_stream, cudaStreamNonBlocking, hi));
     for (int i = 0; i < 2; ++i)
         LL_CUDA(cudaEventCreateWithFlags(&ld->packdone[i], cudaEventDisableTiming));
+}
+
+cudaStream_t wire_stream(ll_loader* ld) {
+    if (!ld->wire_stream) {
+        int lo = 0, hi = 0;
+        LL_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        LL_CUDA(cudaStreamCreateWithPriority(&ld->wire_stream, cudaStreamNonBlocking, hi));
+    }
+    return ld->wire_stream;
 }
 
 // Exchange set `set` (xset[set]) for one step: the pack kernel on the pack
@@ -726,6 +738,7 @@ void loader_destroy(ll_loader* ld) {
     }
     if (ld->side) cudaStreamDestroy(ld->side);
     if (ld->pack_stream) cudaStreamDestroy(ld->pack_stream);
+    if (ld->wire_stream) cudaStreamDestroy(ld->wire_stream);
     for (int i = 0; i < 2; ++i) {
         if (ld->packdone[i]) cudaEventDestroy(ld->packdone[i]);
         if (ld->xdone[i]) cudaEventDestroy(ld->xdone[i]);
@@ -1159,13 +1172,14 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
         } else {
             // not prefetched (first step of an epoch): exchange on the side
             // stream into this slot's buffers, after the step that last read them
-            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[slot], 0));
+            cudaStream_t ws = wire_stream(ld);
+            LL_CUDA(cudaStreamWaitEvent(ws, ld->augdone[slot], 0));
             auto [mv, off, kept, nm, st] = tables(step);
             (void)kept;
             (void)st;
             issue_exchange(ld, ld->plan().view(), epoch, step, mv, nm, off, regcnt(step),
-                           static_cast<int>(slot), ld->side);
-            LL_CUDA(cudaEventRecord(ld->xdone[slot], ld->side));
+                           static_cast<int>(slot), ws);
+            LL_CUDA(cudaEventRecord(ld->xdone[slot], ws));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[slot], 0));
         }
         pend.valid = false;
@@ -1235,13 +1249,14 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
         if (step + 1 < ld->steps) {
             // prefetch the next step's exchange while this augment runs
             const uint32_t ns = (step + 1) & 1;
-            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[ns], 0));
+            cudaStream_t ws = wire_stream(ld);
+            LL_CUDA(cudaStreamWaitEvent(ws, ld->augdone[ns], 0));
             auto [mv, off, kept, nm, st] = tables(step + 1);
             (void)kept;
             (void)st;
             issue_exchange(ld, ld->plan().view(), epoch, step + 1, mv, nm, off, regcnt(step + 1),
-                           static_cast<int>(ns), ld->side);
-            LL_CUDA(cudaEventRecord(ld->xdone[ns], ld->side));
+                           static_cast<int>(ns), ws);
+            LL_CUDA(cudaEventRecord(ld->xdone[ns], ws));
             ld->xpending[ns] = {true, epoch, step + 1};
         }
     }
@@ -1380,11 +1395,12 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
                 }
             }
             xs = static_cast<int>(ld->submitted & 1);
-            LL_CUDA(cudaStreamWaitEvent(ld->side, ld->augdone[xs], 0));
+            cudaStream_t ws = wire_stream(ld);
+            LL_CUDA(cudaStreamWaitEvent(ws, ld->augdone[xs], 0));
             // a loader_step prefetch parked in this set is clobbered now
             ld->xpending[xs].valid = false;
-            issue_exchange(ld, pd, epoch, 0, t->moves, t->n, t->off, rc, xs, ld->side, h.pro_done);
-            LL_CUDA(cudaEventRecord(ld->xdone[xs], ld->side));
+            issue_exchange(ld, pd, epoch, 0, t->moves, t->n, t->off, rc, xs, ws, h.pro_done);
+            LL_CUDA(cudaEventRecord(ld->xdone[xs], ws));
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[xs], 0));
             pre = &ld->xset[xs];
         }
