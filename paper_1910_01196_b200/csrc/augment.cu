@@ -596,25 +596,10 @@ __device__ __forceinline__ void bilerp_g(const uint8_t* base, uint32_t x3, uint3
 // word holding tap a's first byte, `sel` = its byte phase, both per-column
 // constants.  The third word is read unconditionally (its bytes only matter
 // when sel = 3); shards and pull slots carry 16 bytes of tail slack for it.
-// tap word load (variant builds: -DLL_K7_TAP_HINT=1 evict_last, 2 evict_first)
-__device__ __forceinline__ uint32_t ld_tap(const uint32_t* q) {
-#if defined(LL_K7_TAP_HINT) && LL_K7_TAP_HINT == 1
-    uint32_t r;
-    asm volatile("ld.global.nc.L1::evict_last.u32 %0, [%1];" : "=r"(r) : "l"(q));
-    return r;
-#elif defined(LL_K7_TAP_HINT) && LL_K7_TAP_HINT == 2
-    uint32_t r;
-    asm volatile("ld.global.nc.L1::evict_first.u32 %0, [%1];" : "=r"(r) : "l"(q));
-    return r;
-#else
-    return __ldg(q);
-#endif
-}
-
 __device__ __forceinline__ void row_taps_a(const uint8_t* p, uint32_t sel, uint32_t* rg,
                                            uint32_t* bb) {
     const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
-    const uint32_t w0 = ld_tap(q), w1 = ld_tap(q + 1), w2 = ld_tap(q + 2);
+    const uint32_t w0 = __ldg(q), w1 = __ldg(q + 1), w2 = __ldg(q + 2);
     const uint32_t ta = f4e(w0, w1, sel), tb = f4e(w1, w2, sel);  // [Ra Ga Ba Rb] [Gb Bb - -]
     *rg = __byte_perm(ta, tb, 0x4130);
     *bb = __byte_perm(ta, tb, 0x0052);
