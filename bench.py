@@ -538,7 +538,9 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         pinned_ids = torch.empty(B, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
-        k_e2e = min(args.steps, 2 * spe)
+        # at least one epoch, so the prefetch pipeline's fill and drain (depth 4)
+        # do not dominate a short run (the driver's 20 steps)
+        k_e2e = min(max(args.steps, spe), 2 * spe)
         depth = cfg.prefetch_depth
         h2d = d2h = 0
         # warm-up of the host path (pinned slots, side stream, first launches)
