@@ -905,3 +905,88 @@ def test_torch_handoff_zero_copy_train_step(dtype):
     loss.backward()
     assert torch.isfinite(loss).item()
     assert all(p.grad is not None for p in net.parameters())
+
+
+# ------------------------------------------------- HBM sample store (SampleCache)
+def _store(capacity):
+    import ctypes as C
+    h = C.c_void_p()
+    _capi.check(_capi.lib().ll_store_create(C.byref(h), 0, capacity))
+    return h
+
+
+def _store_insert(h, ids, samples):
+    import ctypes as C
+    ids = np.ascontiguousarray(ids, np.uint64)
+    ptrs = (C.c_void_p * len(ids))(*[s.ctypes.data for s in samples])
+    ins = np.zeros(len(ids), np.uint8)
+    _capi.check(_capi.lib().ll_store_insert(h, ll.locload.context(), _capi.ptr(ids, C.c_uint64),
+                                            len(ids), samples[0].size, ptrs,
+                                            _capi.ptr(ins, C.c_uint8)))
+    return ins
+
+
+def test_store_populate_on_first_touch_no_replacement():
+    """ll_store_* = SampleCache (pipeline.hpp:68-94) in HBM: inserts beyond the
+    capacity are skipped, a held id is never replaced, lookups and gathers
+    return the inserted bytes, a gather of an absent id is refused."""
+    import ctypes as C
+    rng = np.random.default_rng(5)
+    S = 3 * 250 * 250  # not a multiple of 16
+    samples = [rng.integers(0, 256, S, dtype=np.uint8) for _ in range(6)]
+    h = _store(4)
+    try:
+        assert _store_insert(h, [10, 11, 12], samples[:3]).tolist() == [1, 1, 1]
+        # 11 again (other bytes): no replacement; 13 fits; 14 is past capacity
+        assert _store_insert(h, [11, 13, 14], samples[3:6]).tolist() == [0, 1, 0]
+        n = C.c_uint64()
+        _capi.check(_capi.lib().ll_store_size(h, C.byref(n)))
+        assert n.value == 4
+        ids = np.array([13, 10, 11, 12, 14, 99], np.uint64)
+        found = np.zeros(len(ids), np.uint8)
+        _capi.check(_capi.lib().ll_store_lookup(h, _capi.ptr(ids, C.c_uint64), len(ids),
+                                                _capi.ptr(found, C.c_uint8)))
+        assert found.tolist() == [1, 1, 1, 1, 0, 0]
+        out = np.empty(4 * S, np.uint8)
+        _capi.check(_capi.lib().ll_store_gather(h, ll.locload.context(),
+                                                _capi.ptr(ids, C.c_uint64), 4,
+                                                _capi.ptr(out, C.c_uint8)))
+        want = [samples[4], samples[0], samples[1], samples[2]]
+        for k in range(4):
+            assert np.array_equal(out[k * S:(k + 1) * S], want[k]), k
+        with pytest.raises(_capi.InvalidArgument, match="not held"):
+            _capi.check(_capi.lib().ll_store_gather(h, ll.locload.context(),
+                                                    _capi.ptr(ids[4:], C.c_uint64), 1,
+                                                    _capi.ptr(out, C.c_uint8)))
+        with pytest.raises(_capi.InvalidArgument, match="same size"):
+            _store_insert(h, [50], [np.zeros(16, np.uint8)])
+    finally:
+        _capi.lib().ll_store_destroy(h)
+
+
+def test_store_zero_capacity_and_many_slabs():
+    """Capacity 0 never holds anything; 3,000 samples of 1 MB span three
+    1-GiB slabs and all gather back intact."""
+    import ctypes as C
+    h = _store(0)
+    try:
+        assert _store_insert(h, [1], [np.ones(64, np.uint8)]).tolist() == [0]
+    finally:
+        _capi.lib().ll_store_destroy(h)
+    S = 1 << 20
+    h = _store(3000)
+    try:
+        base = np.arange(S, dtype=np.uint32).astype(np.uint8)
+        for c0 in range(0, 3000, 500):
+            ids = np.arange(c0, c0 + 500, dtype=np.uint64)
+            samples = [np.roll(base, int(i)) for i in ids]
+            assert _store_insert(h, ids, samples).all()
+        ids = np.array([0, 1023, 1024, 2047, 2048, 2999], np.uint64)
+        out = np.empty(len(ids) * S, np.uint8)
+        _capi.check(_capi.lib().ll_store_gather(h, ll.locload.context(),
+                                                _capi.ptr(ids, C.c_uint64), len(ids),
+                                                _capi.ptr(out, C.c_uint8)))
+        for k, i in enumerate(ids):
+            assert np.array_equal(out[k * S:(k + 1) * S], np.roll(base, int(i))), i
+    finally:
+        _capi.lib().ll_store_destroy(h)
