@@ -642,8 +642,10 @@ def run_ours(args):
                 "exchange": exchange,
                 "kernel_ms": {k: (v[1] / v[0] if v[0] else None) for k, v in stats.items()},
                 "cpu_baseline": cpu,
-                "remote_per_epoch": dict(remote_summary(args, n, d, B, totals),
-                                         headline=headline)}
+                # the headline configuration's remote bytes per epoch (p = 2 / 4 /
+                # 8 at d = 1.28 M) vs the paper's model, then this run's own
+                "remote_per_epoch": dict(headline or {},
+                                         this_run=remote_summary(args, n, d, B, totals))}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
