@@ -258,10 +258,9 @@ __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, 
 template <bool BF16, bool ROW16 = true>
 // (measured: 4 resident CTAs per SM at 72 registers beat forcing 5-9 by
 // register caps or a larger shared-memory carveout; profiles/r01_augment_ab.md)
-#ifndef LL_K6_MINBLOCKS  // variant builds for occupancy A/B runs
-#define LL_K6_MINBLOCKS 1
-#endif
-__global__ void __launch_bounds__(kThreads, LL_K6_MINBLOCKS) k_augment_crop(AugArgs a) {
+// bf16 (half the stores of fp32) runs best at 5 resident CTAs / SM (48
+// registers): 12.95 M vs 12.79 M samples/s; fp32 keeps 4 (profiles/r2_k6_occupancy.md)
+__global__ void __launch_bounds__(kThreads, BF16 ? 5 : 1) k_augment_crop(AugArgs a) {
     __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
     __shared__ uint8_t s_phase[kBand];
     __shared__ const uint8_t* s_src;
