@@ -1187,7 +1187,17 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
     }
     // resize (K7): the prologue of this step was prefetched under the previous
     // step's augment, or runs now; that of the next step is issued after it
-    const bool rpre = c.augment.mode == LL_AUG_RESIZE && !nccl;
+    const bool rpre = c.augment.mode == LL_AUG_RESIZE;
+    // NCCL: the prologue only computes where a received sample's window will
+    // sit (its slot in the step's receive set, xset[step & 1]); it reads no
+    // received bytes, so it may run before the send/recv completes
+    auto with_recv = [&](StepSrc ss, uint64_t st) {
+        if (nccl && (ss.n_send || ss.n_recv)) {
+            ss.src.recv = ld->xset[st & 1].recv.as<uint8_t>();
+            ss.src.recv_slot = msg_slot(ld);
+        }
+        return ss;
+    };
     int pslot = -1;
     if (rpre) {
         if (!ld->rready[0]) {
@@ -1206,7 +1216,8 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
         } else {
             auto [mv, off, kept, nm, st] = tables(step);
             (void)st;
-            const StepSrc ss = step_src(ld, ld->plan().view(), step, mv, off, kept, nm);
+            const StepSrc ss =
+                with_recv(step_src(ld, ld->plan().view(), step, mv, off, kept, nm), step);
             if (resize_prepare(ctx, c.augment, c.seed, epoch, ss.src, ss.n_local, geom_h(c),
                                geom_w(c), rs, ld->tag))
                 pslot = rs;
@@ -1224,7 +1235,8 @@ void loader_step(ll_loader* ld, uint64_t epoch, uint64_t step, ll_step_info* inf
             const int ns = static_cast<int>((step + 1) & 1);
             auto [mv, off, kept, nm, st] = tables(step + 1);
             (void)st;
-            const StepSrc ss = step_src(ld, ld->plan().view(), step + 1, mv, off, kept, nm);
+            const StepSrc ss =
+                with_recv(step_src(ld, ld->plan().view(), step + 1, mv, off, kept, nm), step + 1);
             // set ns was last read by step - 1's augment
             LL_CUDA(cudaStreamWaitEvent(ld->side, ld->rdone[ns], 0));
             cudaStream_t main = ctx->stream;

@@ -28,7 +28,7 @@ are torch.distributed's (NCCL on GPUs, gloo on CPU for the host-logic tests).
 from __future__ import annotations
 
 import ctypes as C
-from typing import Callable, List, Optional
+from typing import List, Optional
 
 import numpy as np
 
@@ -143,9 +143,9 @@ class DistributedTrainer:
         self.ops = ops
 
     # -- collectives ---------------------------------------------------------
-    def _all_gather_rows(self, t, like):
+    def _all_gather_rows(self, t):
         """All-gather a [rows][...] tensor with rows varying per rank."""
-        torch = __import__("torch")
+        import torch
         if self.world == 1:
             return t
         n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
@@ -167,14 +167,14 @@ class DistributedTrainer:
             ids = ops.ids(np.concatenate([lists[j] for j in self.mine]) if self.mine else
                           np.zeros(0, np.int64))
             G = ops.grads(w, ids)
-            all_ids = self._all_gather_rows(ids, ids)
-            all_G = self._all_gather_rows(G, G)
+            all_ids = self._all_gather_rows(ids)
+            all_G = self._all_gather_rows(G)
             return ops.ordered_sum(all_G, ops.argsort(all_ids))
+        import torch
         partials = [ops.ordered_sum(ops.grads(w, ops.ids(lists[j]))) for j in self.mine]
-        torch = __import__("torch")
         if self.agg == "learner_order":
             P = torch.stack(partials)
-            return ops.ordered_sum(self._all_gather_rows(P, P))
+            return ops.ordered_sum(self._all_gather_rows(P))
         mine = ops.ordered_sum(torch.stack(partials))
         if self.world > 1:
             self.dist.all_reduce(mine, op=self.dist.ReduceOp.SUM, group=self.group)
