@@ -148,13 +148,18 @@ def test_four_learners_exchange(tmp_path, exchange, scheme):
 
 
 @pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("exchange,scheme", [("nccl", "locality_balanced"),
-                                             ("nccl", "regular"),
-                                             ("p2p", "locality_balanced")])
-def test_two_learners_host_path(tmp_path, exchange, scheme):
+@pytest.mark.parametrize("exchange,scheme,opts", [
+    ("nccl", "locality_balanced", None), ("nccl", "regular", None),
+    ("p2p", "locality_balanced", None),
+    ("nccl", "locality_balanced", {"alpha": 0.5}), ("nccl", "regular", {"alpha": 0.5}),
+    ("nccl", "locality_balanced", {"variable": True, "d_per": 3000, "b_per": 128})],
+    ids=["nccl-bal", "nccl-reg", "p2p-bal", "nccl-bal-storage", "nccl-reg-storage",
+         "nccl-bal-variable"])
+def test_two_learners_host_path(tmp_path, exchange, scheme, opts):
     """The reference-facing host call (GlobalBatch from host memory, two steps
-    in flight) with the exchange: same outputs as the device-driven steps."""
-    _run(tmp_path, 2, exchange, "bf16", scheme, host=True)
+    in flight) with the exchange: same outputs as the device-driven steps,
+    also with the storage tier and with variable-size sources over NCCL."""
+    _run(tmp_path, 2, exchange, "bf16", scheme, host=True, opts=opts)
 
 
 @pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs")
