@@ -10,6 +10,7 @@
 #include "locload/balance.hpp"
 #include "locload/core.hpp"
 #include "locload/gpu.hpp"
+#include "locload/pipeline.hpp"
 #include "locload/sampling.hpp"
 
 using namespace locload;
@@ -91,4 +92,24 @@ TEST_CASE("device loader rejects bad configurations with the reference messages"
     c.batch_size = 5000;
     CHECK_THROWS_WITH_AS(gpu::DeviceLoader{c}, doctest::Contains("batches: batch size"),
                          std::invalid_argument);
+}
+
+TEST_CASE("SampleCache holds its payloads in HBM: first touch, no replacement, host copies") {
+    SampleCache cache(2);
+    auto make = [](std::uint8_t v, std::size_t n) {
+        return std::make_shared<const std::vector<std::uint8_t>>(n, v);
+    };
+    const std::size_t S = 3 * 250 * 250;  // not a multiple of 16
+    cache.insert(7, make(1, S));
+    cache.insert(9, make(2, S));
+    cache.insert(7, make(3, S));  // already held: not replaced
+    cache.insert(11, make(4, S));  // over capacity: skipped
+    CHECK(cache.size() == 2);
+    CHECK(cache.capacity() == 2);
+    const SampleBytes a = cache.find(7), b = cache.find(9), c = cache.find(11);
+    REQUIRE(a != nullptr);
+    REQUIRE(b != nullptr);
+    CHECK(c == nullptr);
+    CHECK(*a == std::vector<std::uint8_t>(S, 1));
+    CHECK(*b == std::vector<std::uint8_t>(S, 2));
 }
