@@ -2,7 +2,6 @@
 every learner's delivered batch checked against the oracle.  Needs >= 2 GPUs
 (skipped otherwise)."""
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -10,22 +9,19 @@ import pytest
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
+def _rdzv(tmp_path) -> str:
+    """A fresh file:// rendezvous for torch.distributed (no TCP port to race
+    for between tests)."""
+    import uuid
+    return "file://" + str(tmp_path / f"rdzv_{uuid.uuid4().hex}")
 
 
-def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanced",
+def _worker(rank, world, rdzv, exchange, dtype, out_dir, scheme="locality_balanced",
             host=False, opts=None):
     """opts: alpha (storage tier for ids >= alpha*d), hw (fixed source
     geometry, default 256x256), variable (cfg5 geometry, resize mode)."""
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world))
     import torch
     import torch.distributed as dist
     import oracle
@@ -35,7 +31,7 @@ def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanc
     H, W = opts.get("hw", (256, 256))
     variable = opts.get("variable", False)
     torch.cuda.set_device(rank)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=rdzv, rank=rank, world_size=world)
     d, B, seed = opts.get("d_per", 6000) * world, opts.get("b_per", 192) * world, 42
     aug = AugmentConfig(mode="resize" if variable else "crop", out_dtype=dtype)
     ld = DeviceLoader(LoaderConfig(d=d, height=H, width=W, learners=world, rank=rank,
@@ -105,7 +101,7 @@ def _worker(rank, world, port, exchange, dtype, out_dir, scheme="locality_balanc
 
 def _run(tmp_path, world, exchange, dtype, scheme="locality_balanced", host=False, opts=None):
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(world, _free_port(), exchange, dtype, str(tmp_path), scheme, host,
+    mp.spawn(_worker, args=(world, _rdzv(tmp_path), exchange, dtype, str(tmp_path), scheme, host,
                             opts), nprocs=world, join=True)
     total_recv = wire = 0
     for r in range(world):
@@ -194,16 +190,15 @@ def test_two_learners_nccl_small_sources(tmp_path, hw):
     _run(tmp_path, 2, "nccl", "bf16", "regular", opts={"hw": hw})
 
 
-def _train_worker(rank, world, port, out_dir):
+def _train_worker(rank, world, rdzv, out_dir):
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
     from paper_1910_01196_b200 import locload as ll
     from paper_1910_01196_b200.train_dist import DistributedTrainer
     torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world,
+    dist.init_process_group("nccl", init_method=rdzv, rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
     obj = ll.ToyObjective.synthesize(4096, 16, 7)
     for i, (scheme, agg) in enumerate([("locality_balanced", "canonical"),
@@ -227,7 +222,7 @@ def test_distributed_trainer_nccl_vs_reference(tmp_path):
     import torch.multiprocessing as mp
     import oracle
     world = 2
-    mp.spawn(_train_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_train_worker, args=(world, _rdzv(tmp_path), str(tmp_path)), nprocs=world, join=True)
     for i, (scheme, agg) in enumerate([("locality_balanced", "canonical"),
                                        ("regular", "learner_order"),
                                        ("locality", "canonical"),

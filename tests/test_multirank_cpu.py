@@ -13,7 +13,6 @@ without communicating (digest all-gather) and the max-over-ranks timing rule.
 import ctypes as C
 import hashlib
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -22,15 +21,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAMPLE = 3 * 16 * 16  # small synthetic samples keep the test in seconds
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
+def _rdzv(tmp_path) -> str:
+    """A fresh file:// rendezvous for torch.distributed (no TCP port to race
+    for between tests)."""
+    import uuid
+    return "file://" + str(tmp_path / f"rdzv_{uuid.uuid4().hex}")
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, rdzv, out_dir):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -38,8 +36,7 @@ def _worker(rank, world, port, out_dir):
     import oracle
     from paper_1910_01196_b200 import _capi
 
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=rdzv, rank=rank, world_size=world)
     d, B, seed = 4000, 200, 7
     cached = d
     first = oracle.owned_begin(rank, world, cached)
@@ -105,7 +102,7 @@ def _worker(rank, world, port, out_dir):
 def test_two_rank_exchange_over_gloo(tmp_path):
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _rdzv(tmp_path), str(tmp_path)), nprocs=world, join=True)
     total = 0
     for r in range(world):
         lines = open(tmp_path / f"rank{r}.txt").read().splitlines()

@@ -13,7 +13,6 @@ under the NCCL-style all-reduce they agree to rounding.  The device kernels
 behind the same protocol are covered by tests/test_gpu_train.py.
 """
 import os
-import socket
 
 import numpy as np
 import pytest
@@ -22,12 +21,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 N, DIMS, OBJ_SEED, SEED, LR = 640, 6, 3, 11, 0.05
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    return port
+def _rdzv(tmp_path) -> str:
+    """A fresh file:// rendezvous for torch.distributed (no TCP port to race
+    for between tests)."""
+    import uuid
+    return "file://" + str(tmp_path / f"rdzv_{uuid.uuid4().hex}")
 
 
 class RefOps:
@@ -84,14 +82,13 @@ class RefOps:
         return contextlib.nullcontext()
 
 
-def _worker(rank, world, port, cases, out_dir):
+def _worker(rank, world, rdzv, cases, out_dir):
     import sys
     sys.path.insert(0, ROOT)
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist
     from paper_1910_01196_b200.locload import ToyObjective
     from paper_1910_01196_b200.train_dist import DistributedTrainer
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", init_method=rdzv, rank=rank, world_size=world)
     obj = ToyObjective.synthesize(N, DIMS, OBJ_SEED)  # host-only library call
     for i, (scheme, agg, p, B, steps) in enumerate(cases):
         tr = DistributedTrainer(obj, scheme, p, B, SEED, LR, aggregation=agg,
@@ -112,7 +109,7 @@ def test_distributed_sgd_matches_reference(tmp_path, ref_lib):
     import oracle
     import torch.multiprocessing as mp
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), CASES, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _rdzv(tmp_path), CASES, str(tmp_path)), nprocs=world, join=True)
     for i, (scheme, agg, p, B, steps) in enumerate(CASES):
         ref_agg = "canonical" if agg == "canonical" else "learner_order"
         want_w, want_g = oracle.ref_run_training(N, DIMS, OBJ_SEED, scheme, p, B, steps, SEED,
