@@ -617,7 +617,10 @@ def run_ours(args):
                    "note": "zero-copy reads of the crop windows by the augment kernel"}
     headline = None
     if rank == 0 and not os.environ.get("LL_BENCH_NO_HEADLINE_PLAN"):
-        headline = headline_remote(local)
+        try:
+            headline = headline_remote(local)
+        except Exception as e:  # never lose the bench line over the side report
+            headline = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": n,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
