@@ -256,11 +256,16 @@ typedef struct ll_loader_config {
     uint32_t learners;        /* p                                             */
     uint32_t rank;            /* this learner                                  */
     uint64_t batch_size;      /* GLOBAL batch, LoaderConfig::batch_size          */
-    double alpha;             /* cached fraction (CacheDirectory)               */
+    double alpha;             /* cached fraction (CacheDirectory); alpha < 1
+                                 keeps ids [alpha*d, d) in a pinned host
+                                 storage tier (fixed geometry; any exchange)   */
     uint64_t seed;            /* run_epoch seed: shuffle + augment streams       */
     uint64_t data_seed;       /* generate_dataset seed                           */
     int32_t scheme;           /* LL_SCHEME_*                                     */
-    int32_t exchange;         /* LL_EXCHANGE_*                                   */
+    int32_t exchange;         /* LL_EXCHANGE_*: P2P (peer HBM read by the
+                                 augment) or NCCL (grouped send/recv of crop /
+                                 resize windows; the regular scheme over NCCL
+                                 needs crop mode)                              */
     uint32_t prefetch_depth;  /* LoaderConfig::prefetch_depth: output ring depth */
     uint32_t geometry;        /* LL_GEOM_FIXED: every sample height x width;
                                  LL_GEOM_VARIABLE: sample id is H x W with
@@ -276,7 +281,8 @@ typedef struct ll_step_info {
     uint64_t kept;            /* of which assembled from its own shard          */
     uint64_t received;        /* of which received from other learners          */
     uint64_t moved_total;     /* samples moved box-wide this step               */
-    uint64_t nvlink_bytes;    /* bytes this learner received over NVLink        */
+    uint64_t nvlink_bytes;    /* bytes this learner received over NVLink: the
+                                 NCCL message slots, or (P2P) the samples      */
     uint64_t uncached;        /* samples of the global batch not cached         */
     uint64_t reg_remote;      /* remote samples the regular scheme would need   */
     uintptr_t device_out;     /* this step's [n_local][3][out_h][out_w] tensor  */
