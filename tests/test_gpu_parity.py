@@ -516,6 +516,27 @@ def test_remote_per_epoch_reference_goldens(golden):
         assert int(plan.totals[3]) == c["reg_remote"], c
 
 
+@pytest.mark.parametrize("scheme,alpha,p,B", [("locality_balanced", 0.4, 3, 999),
+                                               ("locality", 0.75, 5, 640),
+                                               ("regular", 0.5, 4, 512)])
+def test_plan_epoch_partial_cache_vs_oracle(scheme, alpha, p, B):
+    """ll_plan_epoch with alpha < 1 and the other schemes: every step's final
+    lists equal the C oracle's assignment of the same permutation."""
+    d, seed, epoch = 30000, 9, 1
+    plan = ll.plan_epoch(seed, epoch, d, p, B, alpha=alpha, scheme=scheme)
+    order = oracle.permute_epoch(seed, epoch, d)
+    cached = oracle.cached_count(d, alpha)
+    mode = {"regular": oracle.MODE_REGULAR, "locality": oracle.MODE_LOCALITY,
+            "locality_balanced": oracle.MODE_LOCALITY_BALANCED}[scheme]
+    uncached = 0
+    for t in range(plan.steps):
+        r = oracle.assign_step(order[t * B:(t + 1) * B], p, cached, mode)
+        assert np.array_equal(plan.final_ids[t], r["final_ids"]), t
+        assert np.array_equal(plan.final_off[t], r["final_off"]), t
+        uncached += int(np.sum(order[t * B:(t + 1) * B] >= cached))
+    assert int(plan.totals[2]) == uncached
+
+
 def test_plan_epoch_errors():
     with pytest.raises(_capi.InvalidArgument, match="batches: batch size must be in"):
         ll.plan_epoch(1, 0, 10, 2, 11)
