@@ -401,12 +401,15 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    nvl_bytes = [0]
+
     def run_steps(t0, k):
         local_samples = 0
         for t in range(t0, t0 + k):
             e, s = divmod(t, spe)
             info = ld.step(e, s)
             local_samples += info.n_local
+            nvl_bytes[0] += info.nvlink_bytes
         return local_samples
 
     def max_over_ranks(x):
@@ -437,6 +440,7 @@ def run_ours(args):
     # the dominant kernel's time per launch, gaps between launches included:
     # roofline.achieved and value describe the same launches.
     _capi.check(lib.ll_ctx_reset_stats(ctx))
+    nvl_bytes[0] = 0
     launches0 = C.c_uint64()
     _capi.check(lib.ll_ctx_launch_count(ctx, C.byref(launches0)))
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -455,6 +459,7 @@ def run_ours(args):
     ms = max_over_ranks(ms_local)
     total_samples = sum_over_ranks(samples)
     value = total_samples / (ms / 1e3)
+    region_nvl_bytes = nvl_bytes[0]
     e_first, s_first = divmod(start, spe)
     e_last, s_last = divmod(start + args.steps - 1, spe)
     n_plans = sum(1 for t in range(start, start + args.steps) if t % spe == spe // 2)
@@ -488,6 +493,20 @@ def run_ours(args):
     _capi.check(lib.ll_ctx_set_timing(ctx, 0))
     diag_ms = d0.elapsed_time(d1)
     exchange = None
+    if n > 1 and args.exchange == "p2p" and not cfg5:
+        # the fused exchange: crop windows K6 read from peer shards over
+        # NVLink (TMA) inside the augment, per rank per step of value's
+        # region, min over ranks
+        per_step = region_nvl_bytes / args.steps
+        gbs = per_step / (ms_local / args.steps / 1e3) / 1e9
+        gbs = max_over_ranks(-gbs) * -1 if dist is not None else gbs
+        exchange = {"backend": "p2p: TMA reads of peer HBM fused into K6",
+                    "recv_bytes_per_step": per_step, "nvlink_gbs": gbs, "peak_gbs": 900.0,
+                    "frac": gbs / 900.0,
+                    "peak_source": "NVLink 5 nominal, per direction per GPU",
+                    "note": "crop-window bytes read from peers / step time of value's region "
+                            "(the exchange overlaps the local part of the augment), min over "
+                            "ranks"}
     if nccl:
         # NVLink GB/s of the NCCL exchange: message bytes this rank received
         # / time from the grouped send/recv's issue to its completion on the

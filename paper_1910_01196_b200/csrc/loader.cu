@@ -556,9 +556,17 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
         info->received = n_recv;
         info->moved_total = h_stats[0];
         // bytes that crossed NVLink into this learner: NCCL message slots, or
-        // (P2P) the samples' bytes read from peer shards
-        info->nvlink_bytes =
-            nvl_recv * (p > 1 && c.exchange == LL_EXCHANGE_NCCL ? msg_slot(ld) : ld->S);
+        // (P2P, crop mode) the crop windows K6 read from peer shards
+        uint64_t per = ld->S;
+        if (p > 1 && c.exchange == LL_EXCHANGE_NCCL)
+            per = msg_slot(ld);
+        else if (c.augment.mode == LL_AUG_CROP)
+            per = 3ull * c.augment.out_h * c.augment.out_w;
+        // regular scheme over P2P: the box's remote samples of the step
+        // (K4's count) spread over the learners -- no per-learner count exists
+        if (reg && c.exchange == LL_EXCHANGE_P2P && h_stats[3] != 0xFFFFFFFFu)
+            nvl_recv = h_stats[3] / p;
+        info->nvlink_bytes = nvl_recv * per;
         info->uncached = h_stats[2];
         info->reg_remote = h_stats[3] == 0xFFFFFFFFu ? UINT64_MAX : h_stats[3];
         info->device_out = reinterpret_cast<uintptr_t>(out);
