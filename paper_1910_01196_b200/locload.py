@@ -8,7 +8,9 @@ std::invalid_argument -> InvalidArgument (a ValueError) with the reference's
 message text; std::runtime_error -> RuntimeError.
 
 Every function that is part of the hot path runs on the GPU (permute_epoch,
-permutation_prefix, reg_slice, loc_distribution, balance, assign, the loader).
+permutation_prefix, reg_slice, loc_distribution, balance, assign, plan_epoch
+-- a whole epoch's plan, the sampler half of Loader::run_epoch -- and the
+loader).
 Pure closed forms that the reference itself defines inline in its headers
 (CacheDirectory.owner, sampling.hpp:22-25) or as O(p) arithmetic (targets,
 deficit_fraction, counts_with_uncached over an existing distribution) are
