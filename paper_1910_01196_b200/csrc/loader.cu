@@ -516,7 +516,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
               const ll_move* h_moves, const uint32_t* h_off, const uint32_t* h_kept,
               uint32_t h_nmoves, const uint32_t* h_stats, ll_step_info* info,
               const ll_loader::ExSet* prefetched = nullptr, int prepared_slot = -1,
-              const uint32_t* h_regcnt = nullptr) {
+              const uint32_t* h_regcnt = nullptr, const std::string* owner = nullptr) {
     ll_ctx* ctx = ld->ctx;
     const ll_loader_config& c = ld->cfg;
     const uint32_t me = c.rank, p = c.learners;
@@ -547,7 +547,7 @@ void run_step(ll_loader* ld, uint64_t epoch, const PlanDev& pd, uint64_t step,
     void* out = ld->out[ld->out_slot]->ptr;
     ld->out_slot = (ld->out_slot + 1) % ld->out.size();
     augment_device(ctx, c.augment, c.seed, epoch, src, n_local, geom_h(c), geom_w(c), out,
-                   prepared_slot, ld->tag);
+                   prepared_slot, owner ? *owner : ld->tag);
     if (info) {
         info->epoch = epoch;
         info->step = step;
@@ -1424,8 +1424,37 @@ void loader_submit_host(ll_loader* ld, uint64_t epoch, uint64_t step, const uint
             LL_CUDA(cudaStreamWaitEvent(ctx->stream, ld->xdone[xs], 0));
             pre = &ld->xset[xs];
         }
+        // resize: K7's prologue on the side stream too (it needs the tables
+        // and, over NCCL, where the receive slots are -- not their bytes), so
+        // it overlaps the previous step's augment instead of running inline
+        int pslot = -1;
+        if (c.augment.mode == LL_AUG_RESIZE) {
+            StepSrc ss = step_src(ld, pd, 0, t->moves, t->off, t->kept, t->n);
+            if (pre && (ss.n_send || ss.n_recv)) {
+                ss.src.recv = pre->recv.as<uint8_t>();
+                ss.src.recv_slot = msg_slot(ld);
+            }
+            cudaStream_t main_s = ctx->stream;
+            ctx->stream = ld->side;
+            bool ok = false;
+            try {
+                ok = resize_prepare(ctx, c.augment, c.seed, epoch, ss.src, ss.n_local, geom_h(c),
+                                    geom_w(c), 0, h.rtag);
+            } catch (...) {
+                ctx->stream = main_s;
+                throw;
+            }
+            ctx->stream = main_s;
+            if (ok) {
+                cudaEvent_t ev = ctx->take_event();
+                LL_CUDA(cudaEventRecord(ev, ld->side));
+                LL_CUDA(cudaStreamWaitEvent(ctx->stream, ev, 0));
+                ctx->event_pool.push_back(ev);
+                pslot = 0;
+            }
+        }
         run_step(ld, epoch, pd, 0, t->moves, t->off, t->kept, t->n, t->stats, &local, pre,
-                 -1, rc);
+                 pslot, rc, &h.rtag);
         if (xs >= 0) LL_CUDA(cudaEventRecord(ld->augdone[xs], ctx->stream));
         local.h2d_bytes = h.info.h2d_bytes;
         local.d2h_bytes = tab + (rc ? sizeof(uint32_t) * p * p : 0);
