@@ -342,6 +342,13 @@ int ll_loader_wait_host(ll_loader* ld, uint64_t* host_local_ids, ll_step_info* i
 /* host copies of the current epoch plan for step `step` (tests) */
 int ll_loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_t* final_off,
                         uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);
+/* DLPack view (a DLManagedTensor*, DLPack v0.8 ABI) of a step's augmented
+ * batch: kDLCUDA device, float32 or bfloat16, shape [n_local][3][out_h][out_w],
+ * compact -- the zero-copy hand-off to any DLPack consumer (torch, JAX, CuPy,
+ * a C++ trainer).  The memory stays the loader's (valid until prefetch_depth
+ * later steps); the tensor's deleter frees only the view.  Order the
+ * consumer's stream after ll_ctx_stream before reading. */
+int ll_loader_batch_dlpack(ll_loader* ld, const ll_step_info* info, void** out_managed);
 /* per-epoch totals of the current plan: moved, nvlink-moved, uncached, reg_remote */
 int ll_loader_epoch_totals(ll_loader* ld, uint64_t* out4);
 /* NCCL exchange accounting since the last reset: out8 = {steps, bytes sent,

@@ -135,6 +135,7 @@ PROTOTYPES = {
     "ll_loader_plan_step": (C.c_int, [C.c_void_p, C.c_uint64, u64p, u64p, u64p, u64p,
                                       C.POINTER(Move), u32p]),
     "ll_loader_epoch_totals": (C.c_int, [C.c_void_p, u64p]),
+    "ll_loader_batch_dlpack": (C.c_int, [C.c_void_p, C.POINTER(StepInfo), C.POINTER(C.c_void_p)]),
     "ll_loader_exchange_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     "ll_toy_grads_device": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t, C.c_uint32,
                                       C.c_size_t, C.c_size_t, C.c_uint64, C.c_size_t]),

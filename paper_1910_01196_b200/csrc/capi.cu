@@ -36,6 +36,7 @@ void loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint64_
                       uint64_t* kept, uint64_t* counts, ll_move* moves, uint32_t* n_moves);
 void loader_epoch_totals(ll_loader* ld, uint64_t* out4);
 void loader_exchange_stats(ll_loader* ld, double* out8, int reset);
+void loader_batch_dlpack(ll_loader* ld, const ll_step_info* info, void** out);
 // store.cu
 void store_create(ll_store** out, int device, uint64_t capacity_samples);
 void store_destroy(ll_store* st);
@@ -669,6 +670,13 @@ int ll_loader_plan_step(ll_loader* ld, uint64_t step, uint64_t* final_ids, uint6
 }
 int ll_loader_epoch_totals(ll_loader* ld, uint64_t* out4) {
     return guarded([&] { loader_epoch_totals(ld, out4); });
+}
+
+int ll_loader_batch_dlpack(ll_loader* ld, const ll_step_info* info, void** out_managed) {
+    return guarded([&] {
+        require(ld != nullptr, "null loader");
+        loader_batch_dlpack(ld, info, out_managed);
+    });
 }
 
 int ll_loader_exchange_stats(ll_loader* ld, double* out8, int reset) {

@@ -1562,6 +1562,61 @@ void loader_exchange_stats(ll_loader* ld, double* out8, int reset) {
     }
 }
 
+// ---- DLPack view of a step's batch (the C-level trainer hand-off) --------
+// The DLPack (v0.8) ABI, restated: a consumer of another framework takes the
+// tensor without copying; the deleter frees the view only.
+namespace dl {
+struct Device {
+    int32_t device_type;  // kDLCUDA = 2
+    int32_t device_id;
+};
+struct DataType {
+    uint8_t code;  // kDLFloat = 2, kDLBfloat = 4
+    uint8_t bits;
+    uint16_t lanes;
+};
+struct Tensor {
+    void* data;
+    Device device;
+    int32_t ndim;
+    DataType dtype;
+    int64_t* shape;
+    int64_t* strides;
+    uint64_t byte_offset;
+};
+struct Managed {
+    Tensor dl_tensor;
+    void* manager_ctx;
+    void (*deleter)(Managed*);
+};
+struct Holder {
+    Managed m;
+    int64_t shape[4];
+};
+void release(Managed* m) { delete reinterpret_cast<Holder*>(m); }
+} // namespace dl
+
+void loader_batch_dlpack(ll_loader* ld, const ll_step_info* info, void** out) {
+    require(info != nullptr && out != nullptr, "dlpack: null argument");
+    const ll_loader_config& c = ld->cfg;
+    auto* h = new dl::Holder();
+    h->shape[0] = static_cast<int64_t>(info->n_local);
+    h->shape[1] = 3;
+    h->shape[2] = c.augment.out_h;
+    h->shape[3] = c.augment.out_w;
+    h->m.dl_tensor.data = reinterpret_cast<void*>(info->device_out);
+    h->m.dl_tensor.device = dl::Device{2, ld->ctx->device};
+    h->m.dl_tensor.ndim = 4;
+    h->m.dl_tensor.dtype = c.augment.out_dtype == LL_OUT_BF16 ? dl::DataType{4, 16, 1}
+                                                              : dl::DataType{2, 32, 1};
+    h->m.dl_tensor.shape = h->shape;
+    h->m.dl_tensor.strides = nullptr;  // compact row-major
+    h->m.dl_tensor.byte_offset = 0;
+    h->m.manager_ctx = nullptr;
+    h->m.deleter = dl::release;
+    *out = &h->m;
+}
+
 void loader_epoch_totals(ll_loader* ld, uint64_t* out4) {
     require(ld->plan_epoch >= 0, "Loader: no epoch planned");
     for (int k = 0; k < 4; ++k) out4[k] = 0;

@@ -273,6 +273,18 @@ class DeviceLoader:
         torch.cuda.current_stream(dev).wait_stream(loader_stream)
         return t
 
+    def dlpack_batch(self, info: _capi.StepInfo):
+        """The same batch through the C-ABI's DLPack export
+        (ll_loader_batch_dlpack): a "dltensor" PyCapsule any DLPack consumer
+        takes, e.g. torch.utils.dlpack.from_dlpack(capsule).  Order the
+        consumer's stream after stream_ptr() before reading."""
+        out = C.c_void_p()
+        check(_capi.lib().ll_loader_batch_dlpack(self._h, C.byref(info), C.byref(out)))
+        new_capsule = C.pythonapi.PyCapsule_New
+        new_capsule.restype = C.py_object
+        new_capsule.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        return new_capsule(out, b"dltensor", None)
+
     def fetch_ids(self, info: _capi.StepInfo) -> np.ndarray:
         out = np.empty(info.n_local, np.uint32)
         if info.n_local:

@@ -928,6 +928,29 @@ def test_torch_handoff_zero_copy_train_step(dtype):
     assert all(p.grad is not None for p in net.parameters())
 
 
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_dlpack_handoff(dtype):
+    """The C-ABI's DLPack export (ll_loader_batch_dlpack): a framework-neutral
+    zero-copy view of the step's batch, taken here by torch.utils.dlpack."""
+    import torch
+    import torch.utils.dlpack
+    ld = make_learners(4096, 1, 128, dtype=dtype)[0]
+    info = ld.step(0, 5)
+    stream = torch.cuda.ExternalStream(ld.stream_ptr(), device=torch.device("cuda", 0))
+    torch.cuda.current_stream().wait_stream(stream)
+    t = torch.utils.dlpack.from_dlpack(ld.dlpack_batch(info))
+    assert t.shape == (128, 3, 224, 224) and t.is_cuda and t.is_contiguous()
+    assert t.dtype == (torch.float32 if dtype == "fp32" else torch.bfloat16)
+    assert t.data_ptr() == info.device_out
+    host = ld.fetch(info)
+    if dtype == "fp32":
+        assert np.array_equal(t.cpu().numpy(), host)
+    else:
+        assert np.array_equal(t.view(torch.int16).cpu().numpy().view(np.uint16), host)
+    del t  # the view's deleter runs; the loader's memory stays
+    assert np.array_equal(ld.fetch(info), host)
+
+
 # ------------------------------------------------- HBM sample store (SampleCache)
 def _store(capacity):
     import ctypes as C
