@@ -41,6 +41,12 @@ constexpr uint32_t kOut = 224;        // K6 output side (BASELINE configs)
 constexpr uint32_t kBand = 32;        // rows per CTA
 constexpr uint32_t kBands = kOut / kBand;
 constexpr uint32_t kRowSmem = 704;    // >= 672 + 2*15, multiple of 16
+// Peer samples (P2P over NVLink) arrive as ONE bulk copy of the band's
+// contiguous source span (rows at their source pitch) instead of 32 row
+// requests: 11 % more bytes (31 x 768 + 704 vs 32 x 704 at 256 px) in one
+// large request; cfg4 over P2P at N = 2: +1 % (fp32), +3 % (bf16)
+// (profiles/r2_nvlink_modes.md).
+constexpr uint32_t kBandSmem = kBand * 768;
 constexpr uint32_t kThreads = 224;
 
 struct AugArgs {
@@ -72,8 +78,10 @@ __device__ __forceinline__ void st_cs_v4(void* p, uint4 v) {
 // NVLink, or the host storage tier over PCIe).
 __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* id,
                                         const uint8_t** src, bool* far = nullptr,
-                                        bool* win = nullptr) {  // *win: src is a window slot
+                                        bool* win = nullptr,   // *win: src is a window slot
+                                        bool* peer = nullptr) {  // *peer: a peer shard
     if (far) *far = false;
+    if (peer) *peer = false;
     if (win) *win = false;
     const uint64_t slot = m.recv_row ? kWinBytes : (m.recv_slot ? m.recv_slot : m.sample_bytes);
     if (m.kind == 0) {
@@ -116,6 +124,7 @@ __device__ __forceinline__ void resolve(const SrcMap& m, uint64_t k, uint64_t* i
         const uint64_t first = (static_cast<uint64_t>(o) * m.cached + m.p - 1) / m.p;
         *src = m.peers[o] + (m.prefix ? m.prefix[s] - m.prefix[first] : (s - first) * m.sample_bytes);
         if (far) *far = true;
+        if (peer) *peer = true;
     } else {
         *src = m.recv + (k - kept) * slot;
         if (win) *win = m.recv_row != 0 || m.recv_slot != 0;
@@ -174,7 +183,7 @@ __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint6
     constexpr int PX = BF16 ? 8 : 4;
     constexpr int NB = 3 * PX;      // 12 or 24 source bytes
     constexpr int NW = NB / 4 + 1;  // words covering them at any alignment
-    LL_DCHECK(base >= 0 && base + NB <= static_cast<int32_t>(kRowSmem));
+    LL_DCHECK(base >= 0);
     const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (base >> 2);
     const uint32_t sh = 8u * static_cast<uint32_t>(base & 3);
     uint32_t raw[NW];
@@ -219,9 +228,10 @@ __device__ __forceinline__ void emit_run(const uint8_t* row, int32_t base, uint6
 // its smem row (the row was staged from the 16-byte-aligned address at or
 // below its window start); null when every row starts aligned.
 template <bool BF16>
-__device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, uint32_t a0,
-                                          uint64_t k, uint32_t band, const NormConst& nc,
-                                          void* out, const uint8_t* phase = nullptr) {
+__device__ __forceinline__ void emit_band(const uint8_t* rows, uint32_t pitch, const Params& q,
+                                          uint32_t a0, uint64_t k, uint32_t band,
+                                          const NormConst& nc, void* out,
+                                          const uint8_t* phase = nullptr) {
     constexpr uint32_t PX = BF16 ? 8 : 4;
     constexpr uint32_t TPR = kOut / PX;
     const uint32_t tr = threadIdx.x / TPR, tq = threadIdx.x - tr * TPR;
@@ -243,9 +253,9 @@ __device__ __forceinline__ void emit_band(const uint8_t* rows, const Params& q, 
         const uint64_t o = obase + static_cast<uint64_t>(r) * kOut;
         const int32_t b = phase ? base + phase[r] : base;
         if (q.flip)
-            emit_run<BF16, true>(rows + r * kRowSmem, b, mean2, inv2, out, o, plane);
+            emit_run<BF16, true>(rows + r * pitch, b, mean2, inv2, out, o, plane);
         else
-            emit_run<BF16, false>(rows + r * kRowSmem, b, mean2, inv2, out, o, plane);
+            emit_run<BF16, false>(rows + r * pitch, b, mean2, inv2, out, o, plane);
     }
 }
 
@@ -261,7 +271,7 @@ template <bool BF16, bool ROW16 = true>
 // bf16 (half the stores of fp32) runs best at 5 resident CTAs / SM (48
 // registers): 12.95 M vs 12.79 M samples/s; fp32 keeps 4 (profiles/r2_k6_occupancy.md)
 __global__ void __launch_bounds__(kThreads, BF16 ? 5 : 1) k_augment_crop(AugArgs a) {
-    __shared__ __align__(16) uint8_t rows[kBand][kRowSmem];
+    __shared__ __align__(128) uint8_t rows[kBandSmem];
     __shared__ uint8_t s_phase[kBand];
     __shared__ const uint8_t* s_src;
     __shared__ Params s_prm;
@@ -280,16 +290,18 @@ __global__ void __launch_bounds__(kThreads, BF16 ? 5 : 1) k_augment_crop(AugArgs
         if (a.src.kind == 1) {
             const uint64_t kept = a.src.kept_dev ? *a.src.kept_dev : a.src.kept;
             const uint64_t nr = kept < a.n ? a.n - kept : 0;
+            // (interleaving them evenly over the grid instead measured equal:
+            // cfg4 over P2P at N = 2, profiles/r2_nvlink_modes.txt)
             k = kb < nr ? kept + kb : kb - nr;
         }
         s_k = k;
         uint64_t id;
         const uint8_t* src;
-        bool far = false, win = false;
-        resolve(a.src, k, &id, &src, &far, &win);
+        bool far = false, win = false, peer = false;
+        resolve(a.src, k, &id, &src, &far, &win, &peer);
         s_src = src;
         s_win = win;
-        s_host = far;  // peer shard (NVLink) or host storage tier (PCIe)
+        s_host = far ? (peer ? 2u : 1u) : 0u;  // peer shard (NVLink) or host storage tier (PCIe)
         if (s_host) {  // the band comes by TMA (below); waited on after the barrier
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
                              static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar)))
@@ -327,6 +339,9 @@ __global__ void __launch_bounds__(kThreads, BF16 ? 5 : 1) k_augment_crop(AugArgs
     };
     const uint32_t nch = per_row ? nch0 + 1 : nch0;  // <= 44 chunks = kRowSmem
     LL_DCHECK(nch * 16 <= kRowSmem);
+    // peer sample whose band span fits: one bulk request (kBandSmem above)
+    const bool span = s_host == 2u && !per_row && !win && row_bytes % 16 == 0 &&
+                      (kBand - 1) * row_bytes + nch * 16 <= kBandSmem;
     LL_DCHECK(win || (q.y0 + kOut <= a.H && q.x0 + kOut <= a.W));
     if (per_row && tid < kBand)
         s_phase[tid] = static_cast<uint8_t>(
@@ -337,15 +352,25 @@ __global__ void __launch_bounds__(kThreads, BF16 ? 5 : 1) k_augment_crop(AugArgs
         // 0.82 of the measured pinned H2D bandwidth; cfg4 at N = 4: +3 %)
         const uint32_t mb = static_cast<uint32_t>(__cvta_generic_to_shared(&s_mbar));
         if (tid == 0) {
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
-                         "r"(kBand * nch * 16)
-                         : "memory");
-            for (uint32_t r = 0; r < kBand; ++r) {
-                const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&rows[r][0]));
+            const uint32_t dst0 = static_cast<uint32_t>(__cvta_generic_to_shared(rows));
+            if (span) {  // peer: the band's rows as one contiguous request
+                const uint32_t bytes = (kBand - 1) * row_bytes + nch * 16;
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                             "r"(bytes)
+                             : "memory");
                 asm volatile(
-                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                    "l"(row_src(r)), "r"(nch * 16), "r"(mb)
+                    "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst0),
+                    "l"(row_src(0)), "r"(bytes), "r"(mb)
                     : "memory");
+            } else {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb),
+                             "r"(kBand * nch * 16)
+                             : "memory");
+                for (uint32_t r = 0; r < kBand; ++r)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst0 + r * kRowSmem),
+                        "l"(row_src(r)), "r"(nch * 16), "r"(mb)
+                        : "memory");
             }
         }
         uint32_t done = 0;
@@ -369,12 +394,13 @@ __global__ void __launch_bounds__(kThreads, BF16 ? 5 : 1) k_augment_crop(AugArgs
 #pragma unroll
         for (uint32_t i = 0; i < kIters; ++i) {
             const uint32_t t = tid + i * kThreads, r = t / kSlots, c = t - r * kSlots;
-            if (r < kBand && c < nch) *reinterpret_cast<uint4*>(&rows[r][16 * c]) = v[i];
+            if (r < kBand && c < nch) *reinterpret_cast<uint4*>(&rows[r * kRowSmem + 16 * c]) = v[i];
         }
     }
     __syncthreads();
 
-    emit_band<BF16>(&rows[0][0], q, a0, k, band, a.nc, a.out, per_row ? s_phase : nullptr);
+    emit_band<BF16>(rows, span ? row_bytes : kRowSmem, q, a0, k, band, a.nc, a.out,
+                    per_row ? s_phase : nullptr);
 }
 
 // ---- K7: fixed-point bilinear resize (cfg5) ------------------------------

@@ -1,0 +1,25 @@
+# r2ai: K6 peer samples as one contiguous bulk request per band (new default) vs
+# 32 row requests (variants/k6_rowreq.so = the previous build); 2 GPUs, P2P exchange
+cd "$GRAFT_REPO_ROOT" || exit 1
+mkdir -p gpurun_out
+export LL_BENCH_NO_HEADLINE_PLAN=1
+timeout 900 python -m pytest tests/test_gpu_multi.py tests/test_gpu_parity.py -x -q > gpurun_out/r2ai_pytest.log 2>&1; echo rc=$? >> gpurun_out/r2ai_pytest.log
+tail -2 gpurun_out/r2ai_pytest.log
+line() { python -c "
+import json,sys
+l=json.loads(open('/tmp/o.json').read().strip().splitlines()[-1]); x=l.get('exchange') or {}
+print('$1', round(l['value']/1e6,3), round(l['ms_per_step'],4), round(l['roofline']['frac'],3), x.get('nvlink_gbs'), l['clocks']['sm_mhz'])
+" >> gpurun_out/r2ai_ab.txt 2>&1; }
+for i in 1 2; do
+  for v in default k6_rowreq; do
+    L=paper_1910_01196_b200/liblocload_b200.so; [ $v != default ] && L=variants/$v.so
+    for w in "cfg4" "cfg4 --dtype bf16" "cfg2"; do
+      LL_LIB=$L timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+        --master-port 29531 bench.py --gpus 2 --workload $w --steps 312 --no-cpu-baseline --no-e2e > /tmp/o.json 2>>gpurun_out/r2ai.err
+      line "n2-${w// /}-$v"
+    done
+    LL_LIB=$L timeout 600 python bench.py --steps 624 --no-cpu-baseline --no-e2e > /tmp/o.json 2>>gpurun_out/r2ai.err
+    line "n1-cfg2-$v"
+  done
+done
+cat gpurun_out/r2ai_ab.txt
