@@ -53,9 +53,11 @@ inline void cuda_check(cudaError_t e, const char* what) {
 struct DevBuf {
     void* ptr = nullptr;
     size_t bytes = 0;
+    bool borrowed = false;  // memory owned elsewhere (NCCL-registered): never freed here
     void reserve(size_t n) {
         if (n <= bytes) return;
-        if (ptr) cudaFree(ptr);
+        if (ptr && !borrowed) cudaFree(ptr);
+        borrowed = false;
         ptr = nullptr;
         bytes = 0;
         LL_CUDA(cudaMalloc(&ptr, n));
@@ -72,7 +74,8 @@ struct DevBuf {
     template <typename T>
     T* as() const { return static_cast<T*>(ptr); }
     void release() {
-        if (ptr) cudaFree(ptr);
+        if (ptr && !borrowed) cudaFree(ptr);
+        borrowed = false;
         ptr = nullptr;
         bytes = 0;
     }

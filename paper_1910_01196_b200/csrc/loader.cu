@@ -88,6 +88,11 @@ struct ll_loader {
     // NCCL exchange of step t+1 issued on the side stream while step t's
     // augment runs (two buffer sets, alternating by step parity)
     ExSet xset[2];
+    // exchange buffers from ncclMemAlloc, registered with the communicator
+    // (user-buffer registration: NVLink send/recv may copy between them
+    // directly instead of through NCCL's staging FIFO); freed after the
+    // communicator lets go of them
+    std::vector<std::pair<void*, void*>> nccl_mem;  // {ptr, registration handle}
     cudaEvent_t xdone[2] = {nullptr, nullptr}, augdone[2] = {nullptr, nullptr};
     // the pack kernel of a set runs on its own stream, so step t+1's pack
     // overlaps step t's grouped send/recv on the side stream
@@ -764,7 +769,11 @@ void loader_destroy(ll_loader* ld) {
         if (sl.ready) cudaEventDestroy(sl.ready);
     }
     if (ld->plan_stream) cudaStreamDestroy(ld->plan_stream);
-    if (ld->comm) ncclCommDestroy(ld->comm);
+    if (ld->comm) {
+        for (auto& m : ld->nccl_mem) ncclCommDeregister(ld->comm, m.second);
+        ncclCommDestroy(ld->comm);
+    }
+    for (auto& m : ld->nccl_mem) ncclMemFree(m.first);
     delete ld;
 }
 
@@ -790,9 +799,31 @@ void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     // a learner sends count - target <= B - B/p, which exceeds B/p only when
     // it owns over half of a p > 2 batch (need() fails loudly if it ever does)
     const uint64_t max_send = c.augment.mode == LL_AUG_CROP ? B : share;
+    // LL_NCCL_REGISTER=0: plain cudaMalloc buffers (A/B)
+    const char* reg_env = std::getenv("LL_NCCL_REGISTER");
+    const bool reg = !(reg_env && reg_env[0] == '0');
+    auto alloc = [&](ll::DevBuf& b, uint64_t n) {
+        if (!reg) {
+            b.reserve(n);
+            return;
+        }
+        void* ptr = nullptr;
+        void* handle = nullptr;
+        LL_NCCL(ncclMemAlloc(&ptr, n));
+        const ncclResult_t r = ncclCommRegister(ld->comm, ptr, n, &handle);
+        if (r != ncclSuccess) {
+            ncclMemFree(ptr);
+            LL_NCCL(r);
+        }
+        ld->nccl_mem.emplace_back(ptr, handle);
+        b.release();
+        b.ptr = ptr;
+        b.bytes = n;
+        b.borrowed = true;
+    };
     for (ll_loader::ExSet* x : {&ld->xset[0], &ld->xset[1]}) {
-        x->pack.reserve(std::max<uint64_t>(max_send * slot, 16));
-        x->recv.reserve(std::max<uint64_t>((c.scheme == LL_SCHEME_REGULAR ? B : share) * slot, 16));
+        alloc(x->pack, std::max<uint64_t>(max_send * slot, 16));
+        alloc(x->recv, std::max<uint64_t>((c.scheme == LL_SCHEME_REGULAR ? B : share) * slot, 16));
         x->ridx.reserve(sizeof(uint32_t) * std::max<uint64_t>(share, 1));
     }
     LL_CUDA(cudaDeviceSynchronize());
