@@ -779,6 +779,11 @@ void loader_destroy(ll_loader* ld) {
 
 void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     set_device(ld->ctx);
+    // 128 KB NVLink P2P chunks for the exchange (profiles/r2_nccl_exchange.md);
+    // effective only if no communicator of this process has read NCCL's
+    // parameters yet (the Python package sets it at import); a user's own
+    // value wins
+    setenv("NCCL_P2P_NVL_CHUNKSIZE", "131072", 0);
     ncclUniqueId id;
     static_assert(sizeof(id) == 128, "ncclUniqueId size");
     std::memcpy(&id, id128, sizeof(id));
