@@ -22,5 +22,7 @@ run cfg2_nccl --steps ${STEPS:-624} --exchange nccl
 run cfg3 --workload cfg3 --steps ${STEPS:-312}
 run cfg4 --workload cfg4 --steps ${STEPS:-312}
 run cfg4_nccl --workload cfg4 --exchange nccl --steps ${STEPS:-312}
+run cfg4_bf16 --workload cfg4 --dtype bf16 --steps ${STEPS:-312}
+run cfg4_nccl_bf16 --workload cfg4 --dtype bf16 --exchange nccl --steps ${STEPS:-312}
 run cfg5 --workload cfg5 --steps ${STEPS:-312}
 run cfg5_nccl --workload cfg5 --exchange nccl --steps ${STEPS:-312}
