@@ -365,6 +365,11 @@ def run_ours(args):
     dist = None
     if world > 1:
         import torch.distributed as dist
+        if args.workload == "cfg4" and args.exchange == "nccl":
+            # the regular scheme's all-to-all: 128 KB NVLink P2P chunks (the
+            # loader's comm_init asks for the same, but NCCL reads its
+            # parameters once per process, here at the first communicator)
+            os.environ.setdefault("NCCL_P2P_NVL_CHUNKSIZE", "131072")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     d, B = args.per_gpu_d * n, args.per_gpu_batch * n

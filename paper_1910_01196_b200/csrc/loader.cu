@@ -779,11 +779,15 @@ void loader_destroy(ll_loader* ld) {
 
 void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     set_device(ld->ctx);
-    // 128 KB NVLink P2P chunks for the exchange (profiles/r2_nccl_exchange.md);
-    // effective only if no communicator of this process has read NCCL's
-    // parameters yet (the Python package sets it at import); a user's own
-    // value wins
-    setenv("NCCL_P2P_NVL_CHUNKSIZE", "131072", 0);
+    // The regular scheme's full all-to-all (large messages every step) runs
+    // on registered buffers with 128 KB NVLink P2P chunks; the balanced
+    // schemes' few small tail moves keep cudaMalloc buffers and NCCL's
+    // default chunks, which registration and small chunks slowed at N = 4
+    // (profiles/r2_nccl_exchange.md).  The chunk size takes effect only if no
+    // communicator of this process has read NCCL's parameters yet (bench.py
+    // sets it before torch.distributed for cfg4); a user's own value wins.
+    const bool regular = ld->cfg.scheme == LL_SCHEME_REGULAR;
+    if (regular) setenv("NCCL_P2P_NVL_CHUNKSIZE", "131072", 0);
     ncclUniqueId id;
     static_assert(sizeof(id) == 128, "ncclUniqueId size");
     std::memcpy(&id, id128, sizeof(id));
@@ -804,9 +808,9 @@ void loader_comm_init(ll_loader* ld, const uint8_t* id128) {
     // a learner sends count - target <= B - B/p, which exceeds B/p only when
     // it owns over half of a p > 2 batch (need() fails loudly if it ever does)
     const uint64_t max_send = c.augment.mode == LL_AUG_CROP ? B : share;
-    // LL_NCCL_REGISTER=0: plain cudaMalloc buffers (A/B)
+    // LL_NCCL_REGISTER=0 / 1: plain / registered buffers for every scheme (A/B)
     const char* reg_env = std::getenv("LL_NCCL_REGISTER");
-    const bool reg = !(reg_env && reg_env[0] == '0');
+    const bool reg = reg_env && reg_env[0] ? reg_env[0] != '0' : regular;
     auto alloc = [&](ll::DevBuf& b, uint64_t n) {
         if (!reg) {
             b.reserve(n);
