@@ -133,6 +133,17 @@ def test_two_learners_exchange(tmp_path, exchange, dtype, scheme):
     _run(tmp_path, 2, exchange, dtype, scheme)
 
 
+@pytest.mark.skipif(_n_gpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("scheme,register", [("locality_balanced", "1"), ("regular", "0")])
+def test_two_learners_nccl_buffer_kinds(tmp_path, monkeypatch, scheme, register):
+    """The NCCL exchange on the buffer kind its scheme does not use by default
+    (comm_init: registered ncclMemAlloc buffers for the regular scheme,
+    cudaMalloc for the balanced one; LL_NCCL_REGISTER forces either): same
+    outputs against the oracle."""
+    monkeypatch.setenv("LL_NCCL_REGISTER", register)
+    _run(tmp_path, 2, "nccl", "bf16", scheme)
+
+
 @pytest.mark.skipif(_n_gpus() < 4, reason="needs >= 4 GPUs")
 @pytest.mark.parametrize("exchange,scheme", [("p2p", "locality_balanced"),
                                              ("nccl", "locality_balanced"),
