@@ -1,6 +1,6 @@
 # r2aj: K6 peer windows pulled ahead on the side stream (LL_CROP_PULL=1, new
-# (the side-stream pull build measured here was removed afterwards; LL_CROP_PULL no longer exists)
 # default) vs fused TMA reads of peer shards inside K6 (LL_CROP_PULL=0); 2 GPUs
+# (the side-stream pull build measured here was removed afterwards; LL_CROP_PULL no longer exists)
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
 export LL_BENCH_NO_HEADLINE_PLAN=1
